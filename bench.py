@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""ELSA FP32 exact attention on B200 — the driver's benchmark.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl elsa|reference]
+
+Workload (BASELINE.json configs[2], the config its metric is quoted on):
+FP32 attention B=1 H=16 d=dv=64 at n=16384 — one "step" is one full forward
+over the (B, H, n, d) problem. The headline `value` is whole-job TFLOP/s with
+algorithmic flops 2*B*H*n^2*(d+dv) (QK^T + PV, FMA = 2; exps not counted),
+inputs resident in HBM (3 x 67 MB > the 126 MB L2, so consecutive steps do not
+hit in L2). `e2e` is the same metric through the public drop-in
+(`paper_2604_23798_b200.scaled_dot_product_attention`) with pinned host
+buffers: H2D of Q/K/V and D2H of Y inside the timed region. The 1K..16K sweep
+(plus BERT-base and the single-head config) is reported beside it with the
+L2 flushed between timed iterations.
+
+N > 1 (torchrun, one rank per GPU, NCCL): the same problem KV-sharded across
+the ranks (paper_2604_23798_b200.dist: per-chunk (m,S,W) states, one
+all_to_all, fixed (+)-tree merge) — strong scaling of a fixed problem.
+
+`--impl reference` times the reference's own CPU algorithm (the blocked
+scan of scanattn.engine.scan_forward, restated bit-exactly in
+oracle/scan_port.py) on the host cores, on a bounded sample of the same
+workload (whole 64-query tiles), and reports the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("FP32 attention ms & TFLOP/s vs seq len 1K–16K; % of FP32 FFMA peak; "
+          "1/2/4/8 GPU")
+SMS = 148
+FFMA_LANES = 128
+
+
+def flops(b, h, n_q, n_kv, d=64, dv=64):
+    return 2.0 * b * h * n_q * n_kv * (d + dv)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["elsa", "reference"], default="elsa")
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-tiles", type=int, default=0,
+                    help="64-query tiles per CPU sample (0 = one per worker)")
+    ap.add_argument("--cpu-workers", type=int, default=0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.reader = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+        except (OSError, ValueError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.reader.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- helpers
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def ncu_traffic():
+    """dram bytes per launch of the forward kernel from the committed ncu
+    --set full summary (profiles/ncu_fwd_summary.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_fwd_summary.json")
+    try:
+        with open(path) as f:
+            doc = json.load(f)
+        return doc.get("dram_bytes_per_launch"), doc.get("workload")
+    except (OSError, ValueError):
+        return None, None
+
+
+def cpu_baseline_sample(n, heads, batch, tiles, workers):
+    """Reference CPU algorithm (oracle/scan_port.py = engine.scan_forward) on
+    `tiles` whole 64-query tiles of the workload; returns (TFLOP/s, seconds,
+    description)."""
+    import oracle
+
+    Q, K, V = oracle.generate(0, "regular", b=batch, h=heads, n=n, d=64, d_v=64,
+                              dtype=np.float32)
+    rng = np.random.default_rng(0)
+    starts = [(0, int(rng.integers(0, heads)), 64 * int(rng.integers(0, n // 64)))
+              for _ in range(tiles)]
+    t0 = time.perf_counter()
+    oracle.scan_forward_port(Q, K, V, block_size=128, tile_q=64, workers=workers, tiles=starts)
+    dt = time.perf_counter() - t0
+    fl = tiles * flops(1, 1, 64, n)
+    desc = (f"{tiles} x 64-query tiles of B{batch} H{heads} n{n} d64 (reference blocked scan, "
+            f"B=128, tile_q=64, {workers} threads), extrapolated linearly in tiles")
+    return fl / dt / 1e12, dt, desc
+
+
+def _cpu_workers(args):
+    cores = os.cpu_count() or 1
+    # each worker holds ~0.8 GB of (T, n, d_v) scan lanes at n = 16K; bound RAM
+    return args.cpu_workers or max(1, min(cores, 16))
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    workers = _cpu_workers(args)
+    tiles = args.cpu_sample_tiles or workers
+    n, H, B = args.n, args.heads, args.batch
+    for _ in range(args.warmup):
+        cpu_baseline_sample(min(n, 2048), 1, 1, 1, 1)
+    vals, secs = [], []
+    desc = ""
+    for _ in range(args.steps):
+        v, dt, desc = cpu_baseline_sample(n, H, B, tiles, workers)
+        vals.append(v)
+        secs.append(dt)
+    value = float(np.median(vals))
+    full_ms = flops(B, H, n, n) / (value * 1e12) * 1e3
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (scanattn regular generator, seed 0)",
+        "config": {"workload": f"C3 FP32 attention B{B} H{H} n{n} d64 (bounded CPU sample)",
+                   "B": B, "H": H, "n": n, "d": 64, "dv": 64},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": workers, "kind": "port",
+                         "sample": desc, "sample_seconds_median": float(np.median(secs))},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_23798_b200 as elsa
+    from paper_2604_23798_b200 import dist as edist
+
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    B, H, n = args.batch, args.heads, args.n
+    fl = flops(B, H, n, n)
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- inputs (same generator as the reference, tensorio.py:177-195) ----
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234)
+    q = torch.randn(B, H, n, 64, device=dev, generator=gen)
+    k = torch.randn(B, H, n, 64, device=dev, generator=gen)
+    v = torch.randn(B, H, n, 64, device=dev, generator=gen)
+    chunks = 8 if world <= 8 and 8 % world == 0 else world
+    if world > 1:
+        k_loc, v_loc, off = edist.shard_kv(k, v, rank, world, chunks)
+        k_loc, v_loc = k_loc.contiguous(), v_loc.contiguous()
+
+    launches = [0]
+
+    def step():
+        if world == 1:
+            y = elsa.scaled_dot_product_attention(q, k, v)
+            launches[0] += elsa.last_launch_count()
+            return y
+        r = edist.kv_sharded_attention(q, k_loc, v_loc, off, n, chunks=chunks, gather=False)
+        launches[0] += 2 * (chunks // world) + 1
+        return r
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    launches[0] = 0
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_total = e0.elapsed_time(e1)
+    clock_info = clocks.stop()
+    timed_launches = launches[0]
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms = ms_total / args.steps
+    value = fl / (ms * 1e-3) / 1e12
+
+    # ---- e2e through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e and world == 1:
+        hq = q.cpu().pin_memory()
+        hk = k.cpu().pin_memory()
+        hv = v.cpu().pin_memory()
+        hy = torch.empty((B, H, n, 64), dtype=torch.float32).pin_memory()
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+        def e2e_step():
+            dq.copy_(hq, non_blocking=True)
+            dk.copy_(hk, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            y = elsa.scaled_dot_product_attention(dq, dk, dv)
+            hy.copy_(y, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        steps_e2e = max(3, min(args.steps, 10))
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(steps_e2e):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = a0.elapsed_time(a1) / steps_e2e
+        e2e = {"value": fl / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 3 * q.numel() * 4, "d2h_bytes_per_step": hy.numel() * 4,
+               "steps": steps_e2e}
+
+    # ---- roofline: FFMA peak (spec clock) and the K4 microbenchmark ----
+    peaks = measured_peaks()
+    fmax = float(peaks.get("sm_max_mhz", 1965.0))
+    spec_peak = SMS * FFMA_LANES * 2 * fmax * 1e6 / 1e12
+    k4 = None
+    try:
+        k4 = elsa.ffma_peak_tflops(dev)
+    except Exception:  # noqa: BLE001
+        k4 = None
+    traffic, traffic_workload = ncu_traffic()
+    roofline = {
+        "bound": "ffma", "achieved": value, "peak": spec_peak, "unit": "TFLOP/s",
+        "frac": value / spec_peak,
+        "peak_source": f"148 SM x 128 FP32 lanes x 2 x {fmax:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+        "k4_ffma_measured": k4, "frac_of_k4": (value / k4) if k4 else None,
+        "traffic": traffic, "traffic_workload": traffic_workload,
+        "algorithmic_bytes_per_launch": 4 * B * H * (n * 64 * 3 + n * 64),
+        "kernel": "elsa::fwd_f32_kernel<4,64,2,true>",
+        "measurement": "CUDA events on the launching stream around the K timed steps; "
+                       "one kernel launch per step at this shape",
+    }
+
+    # ---- sweep (kernel-only, L2 flushed between iterations) ----
+    sweep = []
+    if not args.no_sweep and world == 1:
+        flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
+        cases = [(1, 16, nn) for nn in (1024, 2048, 4096, 8192, 16384)] + [(8, 12, 512), (1, 1, 1024)]
+        for (bb, hh, nn) in cases:
+            qq = torch.randn(bb, hh, nn, 64, device=dev)
+            kk = torch.randn(bb, hh, nn, 64, device=dev)
+            vv = torch.randn(bb, hh, nn, 64, device=dev)
+            for _ in range(3):
+                elsa.scaled_dot_product_attention(qq, kk, vv)
+            reps = 20 if nn <= 4096 else 6
+            times = []
+            for _ in range(reps):
+                flush.fill_(1.0)
+                s0 = torch.cuda.Event(enable_timing=True)
+                s1 = torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                elsa.scaled_dot_product_attention(qq, kk, vv)
+                s1.record(stream)
+                torch.cuda.synchronize()
+                times.append(s0.elapsed_time(s1))
+            t_ms = float(np.median(times))
+            tf = flops(bb, hh, nn, nn) / (t_ms * 1e-3) / 1e12
+            sweep.append({"B": bb, "H": hh, "n": nn, "ms": t_ms, "tflops": tf,
+                          "frac_ffma_peak": tf / spec_peak,
+                          "kv_splits": elsa.resolve_kv_splits(qq, kk, vv)})
+            del qq, kk, vv
+        # GPU comparator on the same box: torch SDPA FP32 (TF32 off), the paper's ME-SDPA
+        try:
+            torch.backends.cuda.matmul.allow_tf32 = False
+            torch.backends.cudnn.allow_tf32 = False
+            for _ in range(2):
+                torch.nn.functional.scaled_dot_product_attention(q, k, v)
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(3):
+                torch.nn.functional.scaled_dot_product_attention(q, k, v)
+            s1.record(stream)
+            torch.cuda.synchronize()
+            tms = s0.elapsed_time(s1) / 3
+            sweep.append({"comparator": "torch.nn.functional.scaled_dot_product_attention fp32",
+                          "B": B, "H": H, "n": n, "ms": tms, "tflops": fl / (tms * 1e-3) / 1e12})
+        except Exception as exc:  # noqa: BLE001
+            sweep.append({"comparator": "torch sdpa fp32", "error": str(exc)[:200]})
+
+    # ---- CPU baseline: the reference's algorithm on the host cores (rank 0, N=1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = _cpu_workers(args)
+        tiles = args.cpu_sample_tiles or workers
+        val, secs, desc = cpu_baseline_sample(n, H, B, tiles, workers)
+        cpu = {"value": val, "unit": "TFLOP/s", "cores": workers, "kind": "port",
+               "sample": desc, "seconds": secs}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic N(0,1) Q/K/V (torch.randn), resident in HBM",
+            "config": {"workload": f"C3 FP32 attention B{B} H{H} n{n} d64 dv64"
+                                   + (f", KV-sharded over {world} GPUs ({chunks} chunks)"
+                                      if world > 1 else ""),
+                       "B": B, "H": H, "n": n, "d": 64, "dv": 64,
+                       "l2": "inputs 3x%.0f MB > 126 MB L2; sweep flushes L2 (256 MB write) "
+                             "between timed iterations" % (q.numel() * 4 / 1e6),
+                       "parallelism": f"kv-shard{world}" if world > 1 else "single GPU"},
+            "e2e": e2e, "gpu_launches": timed_launches, "clocks": clock_info,
+            "roofline": roofline, "cpu_baseline": cpu, "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,132 @@
+/*
+ * elsa.h — C-ABI of libelsa.so, the B200 (sm_100a) FP32 exact-attention
+ * library that computes softmax(Q K^T * scale) V as an associative
+ * (m, S, W) state reduction (ELSA, arXiv 2604.23798).
+ *
+ * Plain C: no CUDA, torch or C++ types cross this boundary. Device
+ * pointers are raw `float*`; streams are passed as `void*` holding a
+ * `cudaStream_t` (NULL = legacy default stream). All buffers are
+ * caller-owned device memory; the library never allocates on the hot
+ * path. Every entry point is stream-ordered and never synchronises the
+ * host except `elsa_get_device_error` and `elsa_ffma_peak`.
+ *
+ * Reference interface each entry point replaces (the reference package
+ * `scanattn` is pure Python/numpy, /root/reference/pkg/src/scanattn):
+ *
+ *   elsa_fwd_f32      <- engine.scan_forward(problem, cfg)        engine.py:385-427
+ *                        (score-tile producer engine.py:352-358, intra-block
+ *                        scan engine.py:148-176/315-339, inter-block sweep
+ *                        engine.py:179-199, epilogue engine.py:375-382)
+ *   elsa_partial_f32  <- engine.blockwise_states(...) + inter_block_combine
+ *                        engine.py:430-451 / 265-297: the (m, S, W) summary
+ *                        of one contiguous key range (Proposition 1,
+ *                        PAPER.md:662-666) — the per-KV-shard state
+ *   elsa_merge_f32    <- monoid.merge_tree / merge_lanes_into
+ *                        monoid.py:234-265 / 160-200, plus the epilogue
+ *                        W / S with the normalizer check engine.py:377-382
+ *   elsa_scan_depth   <- engine.scan_depth                        engine.py:47-55
+ *   status codes      <- errors.py:8-54 mapped as the CLI does, cli.py:341-354
+ */
+#ifndef ELSA_H_
+#define ELSA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ELSA_ABI_VERSION 1
+
+/* Status codes. 2/3 match the reference CLI's exit codes for ShapeError /
+ * NumericalError (cli.py:344-351). */
+typedef enum {
+  ELSA_OK = 0,
+  ELSA_ERR_SHAPE = 2,      /* bad shape / stride / config  (errors.ShapeError)     */
+  ELSA_ERR_NUMERICAL = 3,  /* normalizer <= 0 or non-finite (errors.NumericalError) */
+  ELSA_ERR_CUDA = 5,       /* CUDA runtime / launch failure                         */
+  ELSA_ERR_NCCL = 6,       /* collective failure (reported by the host layer)       */
+  ELSA_ERR_WORKSPACE = 7   /* workspace missing or too small                        */
+} elsa_status;
+
+/* Problem geometry. Q:(B,H,n_q,d) K:(B,H,n_kv,d) V:(B,H,n_kv,dv) Y:(B,H,n_q,dv).
+ * Strides are in ELEMENTS for the (b, h, row) axes; the last axis of every
+ * tensor must be contiguous (stride 1). d, dv <= 64. */
+typedef struct {
+  int64_t B, H, n_q, n_kv, d, dv;
+  int64_t q_stride[3];
+  int64_t k_stride[3];
+  int64_t v_stride[3];
+  int64_t y_stride[3];
+} elsa_shape;
+
+/* ABI version (ELSA_ABI_VERSION of the built library). */
+int elsa_abi_version(void);
+
+/* Human-readable text for a status code (static storage). */
+const char* elsa_strerror(int status);
+
+/* The reference's depth bound L(n, B) = ceil(log2 min(B,n)) +
+ * 2*ceil(log2 ceil(n/B)) + 3 (engine.py:47-55). Returns -1 for n<1 or B<1. */
+int elsa_scan_depth(int64_t n, int64_t block_size);
+
+/* kv_splits actually used by elsa_fwd_f32 for `requested` (0 = auto:
+ * enough key-range splits to fill the GPU, bounded by the tile count). */
+int elsa_resolve_kv_splits(const elsa_shape* shp, int requested);
+
+/* Workspace bytes elsa_fwd_f32 needs for `kv_splits` (0 = auto). Zero when
+ * the resolved split count is 1. */
+size_t elsa_workspace_bytes(const elsa_shape* shp, int kv_splits);
+
+/* Y = softmax(Q K^T * scale) V, FP32 in, FP32 FFMA arithmetic, FP32 out.
+ * kv_splits: 0 = auto, else the number of contiguous key-range partitions
+ * whose partial states are merged by a fixed balanced tree (bitwise
+ * deterministic for a given split count). Numerical failures (normalizer
+ * <= 0 or non-finite) raise the device error word; read it with
+ * elsa_get_device_error. */
+int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
+                 const elsa_shape* shp, double scale, int kv_splits,
+                 void* workspace, size_t ws_bytes, void* stream);
+
+/* Partial state of keys [kv_begin, kv_end) for every query row:
+ * m[row] (natural-log anchor, -inf for an empty range), S[row], and
+ * W[row*dv + c], rows ordered (b, h, q) densely: row = (b*H + h)*n_q + q.
+ * The triple follows monoid.StateTriple (monoid.py:73-119): S = sum
+ * exp(s - m), W = sum exp(s - m) v. kv_splits/workspace as for elsa_fwd_f32
+ * (internal splits are merged before the state is written). */
+int elsa_partial_f32(const float* q, const float* k, const float* v,
+                     const elsa_shape* shp, double scale,
+                     int64_t kv_begin, int64_t kv_end,
+                     float* m, float* S, float* W,
+                     int kv_splits, void* workspace, size_t ws_bytes,
+                     void* stream);
+
+/* Merge `parts` partial states per row with the reference's balanced
+ * pairwise tree (adjacent pairs, odd tail passes through; monoid.py:234-265)
+ * and its identity-guarded combine (monoid.py:160-200). Inputs are laid out
+ * part-major: m[p*part_stride + row], S[...], W[(p*part_stride + row)*dv + c].
+ * finalize != 0: y[row*dv + c] = W / S (normalizer check as engine.py:377-378).
+ * finalize == 0: writes the merged state to m_out/S_out/W_out. */
+int elsa_merge_f32(const float* m, const float* S, const float* W,
+                   int parts, int64_t rows, int dv, int64_t part_stride,
+                   int finalize, float* y, float* m_out, float* S_out,
+                   float* W_out, void* stream);
+
+/* Synchronises `stream`, returns the device error word (0 = none, else an
+ * elsa_status) through *code, and clears it. */
+int elsa_get_device_error(void* stream, int* code);
+
+/* FFMA roofline microbenchmark (K4): dependent-chain-free FP32 FMA stream on
+ * every SM at the live clock. Writes achieved TFLOP/s (2 flop per FMA). */
+int elsa_ffma_peak(void* stream, double* tflops);
+
+/* Number of kernels the last elsa_fwd_f32 / elsa_partial_f32 call on this
+ * host thread launched (for the bench's gpu_launches accounting). */
+int elsa_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ELSA_H_ */

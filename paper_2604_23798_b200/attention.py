@@ -1,0 +1,270 @@
+"""PyTorch-facing drop-in for the ELSA FP32 exact-attention path.
+
+``scaled_dot_product_attention(q, k, v)`` replaces
+``torch.nn.functional.scaled_dot_product_attention`` on ``(B, H, n, d)`` FP32
+CUDA tensors (the entry point the paper describes, PAPER.md:18, :106-110,
+:894-898) and runs the hand-written sm_100a kernels in ``libelsa.so``. It
+mirrors the reference's computation ``scan_forward`` (engine.py:385-427):
+exact softmax attention with scale ``1/sqrt(d)`` (tensorio.py:109-112),
+strict FP32 arithmetic, deterministic output.
+
+Non-goals of the reference are rejected loudly rather
+than silently routed elsewhere: attention masks, causal masking, dropout,
+non-FP32 dtypes and CPU tensors raise :class:`ShapeError`. There is no CPU or
+PyTorch fallback anywhere on this path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _lib
+from .errors import NumericalError, ShapeError
+
+__all__ = [
+    "scaled_dot_product_attention",
+    "partial_states",
+    "merge_states",
+    "check_device_error",
+    "resolve_kv_splits",
+    "ffma_peak_tflops",
+]
+
+
+def _stream_ptr(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _as_4d(t, name):
+    if not isinstance(t, torch.Tensor):
+        raise ShapeError(f"{name} must be a torch.Tensor")
+    if t.dim() == 4:
+        return t
+    if t.dim() == 3:
+        return t.unsqueeze(1)
+    if t.dim() == 2:
+        return t.unsqueeze(0).unsqueeze(0)
+    if t.dim() > 4:
+        # fold extra leading batch axes into B
+        return t.reshape(-1, t.shape[-3], t.shape[-2], t.shape[-1])
+    raise ShapeError(f"{name} must have at least 2 dimensions, got shape {tuple(t.shape)}")
+
+
+def _validate(q, k, v):
+    for name, t in (("query", q), ("key", k), ("value", v)):
+        if not isinstance(t, torch.Tensor):
+            raise ShapeError(f"{name} must be a torch.Tensor")
+        if t.dtype != torch.float32:
+            raise ShapeError(
+                f"{name} dtype {t.dtype}: the ELSA FP32 path takes torch.float32 only "
+                "(no TF32/FP16 fallback)")
+        if not t.is_cuda:
+            raise ShapeError(f"{name} is on {t.device}: libelsa runs on CUDA devices only "
+                             "(no CPU fallback)")
+    if not (q.device == k.device == v.device):
+        raise ShapeError("query, key and value must be on the same device")
+
+
+def _prep(t):
+    # the ABI needs the last axis contiguous; other axes may be strided views
+    if t.stride(-1) != 1 and t.shape[-1] > 1:
+        t = t.contiguous()
+    return t
+
+
+def _shape(q, k, v, y=None):
+    B, H, n_q, d = q.shape
+    Bk, Hk, n_kv, dk = k.shape
+    Bv, Hv, n_v, dv = v.shape
+    if (Bk, Hk) != (B, H) or (Bv, Hv) != (B, H):
+        raise ShapeError(f"batch/head dims differ: q {tuple(q.shape)}, k {tuple(k.shape)}, "
+                         f"v {tuple(v.shape)}")
+    if dk != d:
+        raise ShapeError(f"key width {dk} != query width {d}")
+    if n_v != n_kv:
+        raise ShapeError(f"value length {n_v} != key length {n_kv}")
+    if n_kv < 1:
+        raise ShapeError("key/value length must be >= 1")
+    if d > 64 or dv > 64:
+        raise ShapeError(f"head dims d={d}, dv={dv}: libelsa supports d, dv <= 64")
+    s = _lib.ElsaShape()
+    s.B, s.H, s.n_q, s.n_kv, s.d, s.dv = B, H, n_q, n_kv, d, dv
+    for dst, t in ((s.q_stride, q), (s.k_stride, k), (s.v_stride, v)):
+        dst[0], dst[1], dst[2] = t.stride(0), t.stride(1), t.stride(2)
+    if y is not None:
+        s.y_stride[0], s.y_stride[1], s.y_stride[2] = y.stride(0), y.stride(1), y.stride(2)
+    return s
+
+
+def check_device_error(device=None):
+    """Synchronise the current stream and raise :class:`NumericalError` if a
+    kernel flagged a zero / non-finite normalizer since the last check
+    (engine.py:377-378)."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    code = ctypes.c_int(0)
+    with torch.cuda.device(dev):
+        _lib.check_status(_lib.lib().elsa_get_device_error(_stream_ptr(dev), ctypes.byref(code)),
+                          "elsa_get_device_error")
+    if code.value == _lib.ELSA_ERR_NUMERICAL:
+        raise NumericalError("softmax normalizer is zero or non-finite; inputs are corrupted")
+    if code.value:
+        _lib.check_status(code.value, "device")
+
+
+def resolve_kv_splits(q, k, v, kv_splits=0):
+    """Split count elsa_fwd_f32 uses for these shapes (0 = auto)."""
+    q4, k4, v4 = _as_4d(q, "query"), _as_4d(k, "key"), _as_4d(v, "value")
+    shp = _shape(q4, k4, v4)
+    with torch.cuda.device(q4.device):
+        r = _lib.lib().elsa_resolve_kv_splits(ctypes.byref(shp), int(kv_splits))
+    if r < 0:
+        _lib.check_status(-r, "elsa_resolve_kv_splits")
+    return r
+
+
+def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.0,
+                                 is_causal=False, scale=None, enable_gqa=False, *,
+                                 kv_splits=0, check_numerics=False, out=None):
+    """Exact FP32 softmax attention, drop-in for
+    ``torch.nn.functional.scaled_dot_product_attention``.
+
+    ``kv_splits`` (keyword-only) sets the number of contiguous key-range
+    partitions merged by the fixed (+)-tree (0 = auto). ``check_numerics``
+    synchronises and raises :class:`NumericalError` on a bad normalizer, the
+    way the reference raises from ``scan_forward`` (engine.py:377-378).
+    """
+    if attn_mask is not None:
+        raise ShapeError("attn_mask is not supported: masks are a non-goal of the ELSA "
+                         "FP32 path (SPEC.md:242)")
+    if dropout_p:
+        raise ShapeError("dropout is not supported on the exact-attention path")
+    if is_causal:
+        raise ShapeError("is_causal is not supported: the reference computes full "
+                         "(bidirectional) attention only")
+    _validate(query, key, value)
+    orig_dim = query.dim()
+    orig_shape = query.shape
+    q, k, v = (_prep(_as_4d(t, n)) for t, n in ((query, "query"), (key, "key"), (value, "value")))
+    if enable_gqa and k.shape[1] != q.shape[1]:
+        raise ShapeError("grouped-query attention (enable_gqa with H_kv != H_q) is not supported")
+    d = q.shape[-1]
+    sc = (1.0 / math.sqrt(d)) if scale is None else float(scale)
+    if not math.isfinite(sc):
+        raise ShapeError(f"scale must be finite, got {sc}")
+    B, H, n_q, _ = q.shape
+    dv = v.shape[-1]
+    if out is None:
+        y = torch.empty((B, H, n_q, dv), device=q.device, dtype=torch.float32)
+    else:
+        y = out
+        if tuple(y.shape) != (B, H, n_q, dv) or y.dtype != torch.float32 or y.device != q.device \
+                or y.stride(-1) != 1:
+            raise ShapeError("out must be a float32 (B, H, n_q, dv) tensor on the input device "
+                             "with a contiguous last axis")
+    shp = _shape(q, k, v, y)
+    h = _lib.lib()
+    with torch.cuda.device(q.device):
+        ws_bytes = h.elsa_workspace_bytes(ctypes.byref(shp), int(kv_splits))
+        ws = torch.empty(max(ws_bytes, 1), device=q.device, dtype=torch.uint8) if ws_bytes else None
+        st = h.elsa_fwd_f32(
+            ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),
+            ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(y.data_ptr()), ctypes.byref(shp),
+            ctypes.c_double(sc), int(kv_splits),
+            ctypes.c_void_p(ws.data_ptr() if ws is not None else 0), ctypes.c_size_t(ws_bytes),
+            _stream_ptr(q.device))
+        _lib.check_status(st, "elsa_fwd_f32")
+        if check_numerics:
+            check_device_error(q.device)
+    if orig_dim == 4 or out is not None:
+        return y
+    return y.reshape(*orig_shape[:-1], dv)
+
+
+def partial_states(query, key, value, kv_begin=0, kv_end=None, scale=None, kv_splits=1):
+    """The (m, S, W) summary of keys ``[kv_begin, kv_end)`` for every query —
+    the per-chunk state of Proposition 1, as
+    ``engine.blockwise_states`` + ``inter_block_combine`` produce on CPU
+    (engine.py:430-451, 265-297). Returns ``m, S`` shaped (B, H, n_q) and
+    ``W`` shaped (B, H, n_q, dv); ``m`` is in natural-log units, -inf for an
+    empty range."""
+    _validate(query, key, value)
+    q, k, v = (_prep(_as_4d(t, n)) for t, n in ((query, "query"), (key, "key"), (value, "value")))
+    B, H, n_q, d = q.shape
+    n_kv, dv = k.shape[2], v.shape[-1]
+    kv_end = n_kv if kv_end is None else int(kv_end)
+    sc = (1.0 / math.sqrt(d)) if scale is None else float(scale)
+    shp = _shape(q, k, v)
+    m = torch.empty((B, H, n_q), device=q.device, dtype=torch.float32)
+    S = torch.empty_like(m)
+    W = torch.empty((B, H, n_q, dv), device=q.device, dtype=torch.float32)
+    h = _lib.lib()
+    with torch.cuda.device(q.device):
+        # workspace for the internal split tree, sized for the requested count
+        ws_bytes = 0
+        if kv_splits != 1:
+            ws_bytes = h.elsa_workspace_bytes(ctypes.byref(shp), int(kv_splits))
+        ws = torch.empty(max(ws_bytes, 1), device=q.device, dtype=torch.uint8) if ws_bytes else None
+        st = h.elsa_partial_f32(
+            ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),
+            ctypes.c_void_p(v.data_ptr()), ctypes.byref(shp), ctypes.c_double(sc),
+            int(kv_begin), int(kv_end), ctypes.c_void_p(m.data_ptr()),
+            ctypes.c_void_p(S.data_ptr()), ctypes.c_void_p(W.data_ptr()), int(kv_splits),
+            ctypes.c_void_p(ws.data_ptr() if ws is not None else 0), ctypes.c_size_t(ws_bytes),
+            _stream_ptr(q.device))
+        _lib.check_status(st, "elsa_partial_f32")
+    return m, S, W
+
+
+def merge_states(m, S, W, finalize=True):
+    """Merge P partial states with the reference's balanced (+)-tree
+    (monoid.py:234-265). ``m, S``: (P, *rows); ``W``: (P, *rows, dv), all FP32
+    CUDA. ``finalize`` returns Y = W / S (*rows, dv); otherwise the merged
+    ``(m, S, W)``."""
+    for name, t in (("m", m), ("S", S), ("W", W)):
+        if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_cuda:
+            raise ShapeError(f"{name} must be a float32 CUDA tensor")
+    P = m.shape[0]
+    rows_shape = tuple(m.shape[1:])
+    dv = W.shape[-1]
+    if tuple(S.shape) != tuple(m.shape) or tuple(W.shape[:-1]) != tuple(m.shape):
+        raise ShapeError("m, S, W shapes disagree")
+    rows = math.prod(rows_shape) if rows_shape else 1
+    mc, Sc, Wc = m.contiguous(), S.contiguous(), W.contiguous()
+    h = _lib.lib()
+    with torch.cuda.device(m.device):
+        if finalize:
+            y = torch.empty((*rows_shape, dv), device=m.device, dtype=torch.float32)
+            st = h.elsa_merge_f32(
+                ctypes.c_void_p(mc.data_ptr()), ctypes.c_void_p(Sc.data_ptr()),
+                ctypes.c_void_p(Wc.data_ptr()), int(P), int(rows), int(dv), int(rows), 1,
+                ctypes.c_void_p(y.data_ptr()), None, None, None, _stream_ptr(m.device))
+            _lib.check_status(st, "elsa_merge_f32")
+            return y
+        mo = torch.empty(rows_shape, device=m.device, dtype=torch.float32)
+        So = torch.empty_like(mo)
+        Wo = torch.empty((*rows_shape, dv), device=m.device, dtype=torch.float32)
+        st = h.elsa_merge_f32(
+            ctypes.c_void_p(mc.data_ptr()), ctypes.c_void_p(Sc.data_ptr()),
+            ctypes.c_void_p(Wc.data_ptr()), int(P), int(rows), int(dv), int(rows), 0, None,
+            ctypes.c_void_p(mo.data_ptr()), ctypes.c_void_p(So.data_ptr()),
+            ctypes.c_void_p(Wo.data_ptr()), _stream_ptr(m.device))
+        _lib.check_status(st, "elsa_merge_f32")
+        return mo, So, Wo
+
+
+def ffma_peak_tflops(device=None):
+    """Run the K4 FFMA microbenchmark on ``device`` and return TFLOP/s."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    out = ctypes.c_double(0.0)
+    with torch.cuda.device(dev):
+        _lib.check_status(_lib.lib().elsa_ffma_peak(_stream_ptr(dev), ctypes.byref(out)),
+                          "elsa_ffma_peak")
+    return out.value
+
+
+def last_launch_count():
+    """Kernels the last libelsa forward/partial/merge call launched on this thread."""
+    return _lib.lib().elsa_last_launch_count()

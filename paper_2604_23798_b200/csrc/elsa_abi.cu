@@ -1,0 +1,574 @@
+// elsa_abi.cu — host side of libelsa.so: argument validation, TMA descriptor
+// encoding, kv-split planning and stream-ordered launches behind the C-ABI
+// declared in include/elsa.h.
+//
+// Reference behaviour mirrored here:
+//   ShapeError on bad geometry/config           errors.py:8, tensorio.py:83-98, engine.py:78-89
+//   NumericalError on a bad normalizer          errors.py:12, engine.py:377-378 (device word)
+//   scan_depth / depth bound                    engine.py:43-55
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "elsa.h"
+#include "ffma_peak.cuh"
+#include "fwd_f32.cuh"
+#include "merge_f32.cuh"
+
+namespace elsa {
+__device__ int g_device_error;
+}
+
+using namespace elsa;
+
+namespace {
+
+constexpr int kMaxDevices = 64;
+constexpr int kMaxSplits = kMergeMaxParts;
+constexpr double kLog2e = 1.4426950408889634074;
+
+thread_local int t_last_launches = 0;
+
+struct DeviceCache {
+  bool ready = false;
+  int sms = 0;
+  int* err = nullptr;
+  bool attr[8] = {};
+};
+DeviceCache g_dev[kMaxDevices];
+std::mutex g_mu;
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode;
+}
+
+int current_device_cache(DeviceCache** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return ELSA_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DeviceCache& c = g_dev[dev];
+  if (!c.ready) {
+    if (cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return ELSA_ERR_CUDA;
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, g_device_error) != cudaSuccess) return ELSA_ERR_CUDA;
+    c.err = static_cast<int*>(p);
+    c.ready = true;
+  }
+  *out = &c;
+  return ELSA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Forward kernel configurations. Selected by ELSA_FWD_CFG (benchmarking aid);
+// the default is the measured best.
+// ---------------------------------------------------------------------------
+enum CfgId { kCfgW4S2 = 0, kCfgW8S2 = 1, kCfgW8S3 = 2, kCfgCount = 3 };
+
+int active_cfg() {
+  static int cfg = [] {
+    const char* e = std::getenv("ELSA_FWD_CFG");
+    if (e && !std::strcmp(e, "w8s2")) return int(kCfgW8S2);
+    if (e && !std::strcmp(e, "w8s3")) return int(kCfgW8S3);
+    return int(kCfgW4S2);
+  }();
+  return cfg;
+}
+
+struct CfgInfo {
+  int tq, tk, ctas_per_sm;
+};
+CfgInfo cfg_info(int cfg) {
+  switch (cfg) {
+    case kCfgW8S2:
+      return {128, 64, 1};
+    case kCfgW8S3:
+      return {128, 64, 1};
+    default:
+      return {64, 64, 2};
+  }
+}
+
+bool valid_shape(const elsa_shape* s) {
+  if (!s) return false;
+  if (s->B < 0 || s->H < 0 || s->n_q < 0 || s->n_kv < 1) return false;
+  if (s->d < 1 || s->d > 64 || s->dv < 1 || s->dv > 64) return false;
+  const int64_t lim = int64_t(1) << 31;
+  if (s->B >= lim || s->H >= lim || s->n_q >= lim || s->n_kv >= lim) return false;
+  if (s->B * s->H >= lim) return false;
+  for (int i = 0; i < 3; ++i)
+    if (s->q_stride[i] < 0 || s->k_stride[i] < 0 || s->v_stride[i] < 0 || s->y_stride[i] < 0)
+      return false;
+  return true;
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Split plan. Cost model in units of one key tile of one CTA:
+//   waves(s) * (ceil(tiles / s) + kCtaOverheadTiles)            forward kernel
+// + [s > 1] * (1 + s * rows * 264 B / kBytesPerTile)            partial-state round trip + merge
+// minimised over s <= min(tiles, 32), with s >= ceil(tiles / kMaxChainTiles) so
+// no CTA folds more than kMaxChainTiles tiles sequentially (bounded chain
+// depth; the rest of the reduction is the log-depth split tree).
+constexpr double kCtaOverheadTiles = 2.0;
+constexpr double kBytesPerTile = 3.0e7;
+constexpr int64_t kMaxChainTiles = 256;
+
+int plan_splits(int64_t ctas, int64_t tiles, int64_t rows, int64_t slots, int requested) {
+  if (tiles < 1) return 1;
+  int64_t s = 1;
+  if (requested > 0) {
+    s = requested;
+  } else {
+    const int64_t smax = tiles < kMaxSplits ? tiles : kMaxSplits;
+    int64_t smin = ceil_div(tiles, kMaxChainTiles);
+    if (smin > smax) smin = smax;
+    double best = 1e300;
+    for (int64_t cand = smin; cand <= smax; ++cand) {
+      double t = double(ceil_div(ctas * cand, slots)) *
+                 (double(ceil_div(tiles, cand)) + kCtaOverheadTiles);
+      if (cand > 1) t += 1.0 + double(cand) * double(rows) * 264.0 / kBytesPerTile;
+      if (t < best - 1e-9) {
+        best = t;
+        s = cand;
+      }
+    }
+  }
+  if (s > tiles) s = tiles;
+  if (s > kMaxSplits) s = kMaxSplits;
+  if (s < 1) s = 1;
+  // drop empty splits: the effective count is ceil(tiles / tiles_per_split)
+  const int64_t tps = ceil_div(tiles, s);
+  return int(ceil_div(tiles, tps));
+}
+
+int resolve_splits_for(const elsa_shape* s, int64_t kv_len, int requested, int sms) {
+  const CfgInfo ci = cfg_info(active_cfg());
+  const int64_t qtiles = ceil_div(s->n_q, ci.tq);
+  const int64_t ctas = qtiles * s->B * s->H;
+  const int64_t tiles = ceil_div(kv_len, ci.tk);
+  if (ctas == 0) return 1;
+  const int64_t rows = s->B * s->H * s->n_q;
+  return plan_splits(ctas, tiles, rows, int64_t(sms) * ci.ctas_per_sm, requested);
+}
+
+// Sanitise the stride of size-1 axes (any value is semantically irrelevant
+// there but TMA wants a positive multiple of 16 bytes).
+void sanitize(int64_t st[3], int64_t rows, int64_t H, int64_t B, int64_t inner) {
+  if (rows == 1 && st[2] == 0) st[2] = inner;
+  if (H == 1) st[1] = st[2] * rows;
+  if (B == 1) st[0] = st[1] * H;
+}
+
+bool tma_ok(const float* base, const int64_t st[3], int64_t inner) {
+  if (reinterpret_cast<uintptr_t>(base) % 16) return false;
+  for (int i = 0; i < 3; ++i) {
+    if (st[i] <= 0 || st[i] % 4) return false;
+    if (st[i] * 4 >= (int64_t(1) << 40)) return false;
+  }
+  (void)inner;
+  return true;
+}
+
+bool encode_map(CUtensorMap* map, const float* base, int64_t inner, int64_t rows, int64_t H,
+                int64_t B, const int64_t st[3], int box_inner, int box_rows) {
+  auto enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {cuuint64_t(inner), cuuint64_t(rows), cuuint64_t(H), cuuint64_t(B)};
+  cuuint64_t strides[3] = {cuuint64_t(st[2] * 4), cuuint64_t(st[1] * 4), cuuint64_t(st[0] * 4)};
+  cuuint32_t box[4] = {cuuint32_t(box_inner), cuuint32_t(box_rows), 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims,
+                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int W, int TK, int ST>
+int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[3],
+                   int64_t v_st[3], int splits, int cfg_slot, DeviceCache* dc,
+                   cudaStream_t stream) {
+  using T = FwdTraits<W, TK, ST>;
+  p.qtiles = int(ceil_div(s->n_q, T::TQ));
+  const int64_t tiles = ceil_div(int64_t(p.kv_end) - p.kv_begin, TK);
+  p.tiles_per_split = int(ceil_div(tiles, splits));
+
+  CUtensorMap maps[3];
+  std::memset(maps, 0, sizeof(maps));
+  bool use_tma = tma_ok(p.q, q_st, s->d) && tma_ok(p.k, k_st, s->d) && tma_ok(p.v, v_st, s->dv);
+  if (use_tma) {
+    use_tma = encode_map(&maps[0], p.q, s->d, s->n_q, s->H, s->B, q_st, T::QP, T::TQ) &&
+              encode_map(&maps[1], p.k, s->d, s->n_kv, s->H, s->B, k_st, T::QP, TK) &&
+              encode_map(&maps[2], p.v, s->dv, s->n_kv, s->H, s->B, v_st, T::VP, TK);
+  }
+  static const bool force_generic = std::getenv("ELSA_FORCE_GENERIC_LOAD") != nullptr;
+  if (force_generic) use_tma = false;
+
+  auto kern = use_tma ? fwd_f32_kernel<W, TK, ST, true> : fwd_f32_kernel<W, TK, ST, false>;
+  const int slot = cfg_slot * 2 + (use_tma ? 1 : 0);
+  if (!dc->attr[slot]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(T::SMEM_BYTES)) != cudaSuccess)
+      return ELSA_ERR_CUDA;
+    dc->attr[slot] = true;
+  }
+  const int64_t gx = int64_t(p.qtiles) * s->B * s->H;
+  if (gx >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
+  const dim3 grid{unsigned(gx), unsigned(splits), 1u};
+  kern<<<grid, T::THREADS, T::SMEM_BYTES, stream>>>(p, maps[0], maps[1], maps[2]);
+  if (cudaPeekAtLastError() != cudaSuccess) {
+    cudaGetLastError();
+    return ELSA_ERR_CUDA;
+  }
+  ++t_last_launches;
+  return ELSA_OK;
+}
+
+int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[3],
+               int64_t v_st[3], int splits, DeviceCache* dc, cudaStream_t stream) {
+  switch (active_cfg()) {
+    case kCfgW8S2:
+      return launch_fwd_cfg<8, 64, 2>(p, s, q_st, k_st, v_st, splits, kCfgW8S2, dc, stream);
+    case kCfgW8S3:
+      return launch_fwd_cfg<8, 64, 3>(p, s, q_st, k_st, v_st, splits, kCfgW8S3, dc, stream);
+    default:
+      return launch_fwd_cfg<4, 64, 2>(p, s, q_st, k_st, v_st, splits, kCfgW4S2, dc, stream);
+  }
+}
+
+int launch_merge(MergeParams& mp, cudaStream_t stream) {
+  if (mp.rows == 0) return ELSA_OK;
+  constexpr int kWarps = 8;
+  const int64_t blocks = ceil_div(mp.rows, kWarps);
+  if (blocks >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
+  merge_f32_kernel<<<unsigned(blocks), kWarps * 32, 0, stream>>>(mp);
+  if (cudaPeekAtLastError() != cudaSuccess) {
+    cudaGetLastError();
+    return ELSA_ERR_CUDA;
+  }
+  ++t_last_launches;
+  return ELSA_OK;
+}
+
+void fill_common(FwdParams& p, const float* q, const float* k, const float* v,
+                 const elsa_shape* s, double scale, const int64_t q_st[3], const int64_t k_st[3],
+                 const int64_t v_st[3]) {
+  std::memset(&p, 0, sizeof(p));
+  p.q = q;
+  p.k = k;
+  p.v = v;
+  p.B = int(s->B);
+  p.H = int(s->H);
+  p.n_q = int(s->n_q);
+  p.n_kv = int(s->n_kv);
+  p.d = int(s->d);
+  p.dv = int(s->dv);
+  p.qs_b = q_st[0];
+  p.qs_h = q_st[1];
+  p.qs_r = q_st[2];
+  p.ks_b = k_st[0];
+  p.ks_h = k_st[1];
+  p.ks_r = k_st[2];
+  p.vs_b = v_st[0];
+  p.vs_h = v_st[1];
+  p.vs_r = v_st[2];
+  p.c = float(scale * kLog2e);
+}
+
+size_t split_ws_bytes(const elsa_shape* s, int splits) {
+  if (splits <= 1) return 0;
+  const size_t rows = size_t(s->B) * size_t(s->H) * size_t(s->n_q);
+  return size_t(splits) * rows * (2 + 64) * sizeof(float);
+}
+
+}  // namespace
+
+extern "C" {
+
+int elsa_abi_version(void) { return ELSA_ABI_VERSION; }
+
+const char* elsa_strerror(int status) {
+  switch (status) {
+    case ELSA_OK:
+      return "ok";
+    case ELSA_ERR_SHAPE:
+      return "shape/config error (unsupported geometry, stride or argument)";
+    case ELSA_ERR_NUMERICAL:
+      return "numerical error: softmax normalizer is zero or non-finite";
+    case ELSA_ERR_CUDA:
+      return "CUDA runtime error";
+    case ELSA_ERR_NCCL:
+      return "NCCL error";
+    case ELSA_ERR_WORKSPACE:
+      return "workspace missing or too small";
+    default:
+      return "unknown elsa status";
+  }
+}
+
+int elsa_scan_depth(int64_t n, int64_t block_size) {
+  if (n < 1 || block_size < 1) return -1;
+  auto clog2 = [](int64_t x) {
+    int r = 0;
+    while ((int64_t(1) << r) < x) ++r;
+    return r;
+  };
+  const int64_t b_eff = block_size < n ? block_size : n;
+  const int64_t blocks = ceil_div(n, block_size);
+  return clog2(b_eff) + 2 * clog2(blocks) + 3;
+}
+
+int elsa_resolve_kv_splits(const elsa_shape* shp, int requested) {
+  if (!valid_shape(shp) || requested < 0) return -ELSA_ERR_SHAPE;
+  DeviceCache* dc = nullptr;
+  int sms = 148;
+  if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
+  return resolve_splits_for(shp, shp->n_kv, requested, sms);
+}
+
+size_t elsa_workspace_bytes(const elsa_shape* shp, int kv_splits) {
+  const int s = elsa_resolve_kv_splits(shp, kv_splits);
+  if (s <= 1) return 0;
+  return split_ws_bytes(shp, s);
+}
+
+int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
+                 const elsa_shape* shp, double scale, int kv_splits, void* workspace,
+                 size_t ws_bytes, void* stream) {
+  t_last_launches = 0;
+  if (!valid_shape(shp) || kv_splits < 0 || !std::isfinite(scale)) return ELSA_ERR_SHAPE;
+  if (!q || !k || !v || !y) return ELSA_ERR_SHAPE;
+  if (shp->y_stride[0] < 0 || shp->y_stride[2] < 0) return ELSA_ERR_SHAPE;
+  if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  cudaStream_t strm = static_cast<cudaStream_t>(stream);
+
+  int64_t q_st[3], k_st[3], v_st[3];
+  std::memcpy(q_st, shp->q_stride, sizeof(q_st));
+  std::memcpy(k_st, shp->k_stride, sizeof(k_st));
+  std::memcpy(v_st, shp->v_stride, sizeof(v_st));
+  sanitize(q_st, shp->n_q, shp->H, shp->B, shp->d);
+  sanitize(k_st, shp->n_kv, shp->H, shp->B, shp->d);
+  sanitize(v_st, shp->n_kv, shp->H, shp->B, shp->dv);
+
+  const int splits = resolve_splits_for(shp, shp->n_kv, kv_splits, dc->sms);
+  FwdParams p;
+  fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
+  p.kv_begin = 0;
+  p.kv_end = int(shp->n_kv);
+  p.err = dc->err;
+  p.y = y;
+  p.ys_b = shp->y_stride[0];
+  p.ys_h = shp->y_stride[1];
+  p.ys_r = shp->y_stride[2];
+  p.y_vec = (reinterpret_cast<uintptr_t>(y) % 16 == 0) && (p.ys_b % 4 == 0) &&
+            (p.ys_h % 4 == 0) && (p.ys_r % 4 == 0);
+
+  if (splits <= 1) {
+    p.mode = kModeFinal;
+    return launch_fwd(p, shp, q_st, k_st, v_st, 1, dc, strm);
+  }
+  const size_t need = split_ws_bytes(shp, splits);
+  if (!workspace || ws_bytes < need) return ELSA_ERR_WORKSPACE;
+  const int64_t rows = shp->B * shp->H * shp->n_q;
+  float* ws = static_cast<float*>(workspace);
+  p.mode = kModePartialLog2;
+  p.pm = ws;
+  p.pS = ws + int64_t(splits) * rows;
+  p.pW = ws + int64_t(splits) * rows * 2;
+  p.part_stride = rows;
+  p.pw_pitch = 64;
+  p.pw_vec = 1;
+  if (int st = launch_fwd(p, shp, q_st, k_st, v_st, splits, dc, strm)) return st;
+
+  MergeParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.m = p.pm;
+  mp.S = p.pS;
+  mp.W = p.pW;
+  mp.parts = splits;
+  mp.rows = rows;
+  mp.dv = int(shp->dv);
+  mp.w_pitch = 64;
+  mp.part_stride = rows;
+  mp.log2_domain = 1;
+  mp.finalize = 1;
+  mp.y = y;
+  mp.H = int(shp->H);
+  mp.n_q = int(shp->n_q);
+  mp.ys_b = shp->y_stride[0];
+  mp.ys_h = shp->y_stride[1];
+  mp.ys_r = shp->y_stride[2];
+  mp.err = dc->err;
+  return launch_merge(mp, strm);
+}
+
+int elsa_partial_f32(const float* q, const float* k, const float* v, const elsa_shape* shp,
+                     double scale, int64_t kv_begin, int64_t kv_end, float* m, float* S,
+                     float* W, int kv_splits, void* workspace, size_t ws_bytes, void* stream) {
+  t_last_launches = 0;
+  if (!valid_shape(shp) || kv_splits < 0 || !std::isfinite(scale)) return ELSA_ERR_SHAPE;
+  if (kv_begin < 0 || kv_end < kv_begin || kv_end > shp->n_kv) return ELSA_ERR_SHAPE;
+  if (!q || !k || !v || !m || !S || !W) return ELSA_ERR_SHAPE;
+  const int64_t rows = shp->B * shp->H * shp->n_q;
+  if (rows == 0) return ELSA_OK;
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  cudaStream_t strm = static_cast<cudaStream_t>(stream);
+
+  int64_t q_st[3], k_st[3], v_st[3];
+  std::memcpy(q_st, shp->q_stride, sizeof(q_st));
+  std::memcpy(k_st, shp->k_stride, sizeof(k_st));
+  std::memcpy(v_st, shp->v_stride, sizeof(v_st));
+  sanitize(q_st, shp->n_q, shp->H, shp->B, shp->d);
+  sanitize(k_st, shp->n_kv, shp->H, shp->B, shp->d);
+  sanitize(v_st, shp->n_kv, shp->H, shp->B, shp->dv);
+
+  const int64_t len = kv_end - kv_begin;
+  int splits = len == 0 ? 1 : resolve_splits_for(shp, len, kv_splits, dc->sms);
+  FwdParams p;
+  fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
+  p.kv_begin = int(kv_begin);
+  p.kv_end = int(kv_end);
+  p.err = dc->err;
+  if (splits <= 1) {
+    p.mode = kModePartialNat;
+    p.pm = m;
+    p.pS = S;
+    p.pW = W;
+    p.part_stride = rows;
+    p.pw_pitch = int(shp->dv);
+    p.pw_vec = (reinterpret_cast<uintptr_t>(W) % 16 == 0) && (shp->dv % 4 == 0);
+    return launch_fwd(p, shp, q_st, k_st, v_st, 1, dc, strm);
+  }
+  const size_t need = split_ws_bytes(shp, splits);
+  if (!workspace || ws_bytes < need) return ELSA_ERR_WORKSPACE;
+  float* ws = static_cast<float*>(workspace);
+  p.mode = kModePartialLog2;
+  p.pm = ws;
+  p.pS = ws + int64_t(splits) * rows;
+  p.pW = ws + int64_t(splits) * rows * 2;
+  p.part_stride = rows;
+  p.pw_pitch = 64;
+  p.pw_vec = 1;
+  if (int st = launch_fwd(p, shp, q_st, k_st, v_st, splits, dc, strm)) return st;
+  MergeParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.m = p.pm;
+  mp.S = p.pS;
+  mp.W = p.pW;
+  mp.parts = splits;
+  mp.rows = rows;
+  mp.dv = int(shp->dv);
+  mp.w_pitch = 64;
+  mp.part_stride = rows;
+  mp.log2_domain = 1;
+  mp.finalize = 0;
+  mp.m_out = m;
+  mp.S_out = S;
+  mp.W_out = W;
+  mp.out_pitch = int(shp->dv);
+  mp.out_log2_to_nat = 1;
+  mp.err = dc->err;
+  return launch_merge(mp, strm);
+}
+
+int elsa_merge_f32(const float* m, const float* S, const float* W, int parts, int64_t rows,
+                   int dv, int64_t part_stride, int finalize, float* y, float* m_out,
+                   float* S_out, float* W_out, void* stream) {
+  t_last_launches = 0;
+  if (parts < 1 || parts > kMergeMaxParts || rows < 0 || dv < 1 || dv > 64) return ELSA_ERR_SHAPE;
+  if (part_stride < rows) return ELSA_ERR_SHAPE;
+  if (!m || !S || !W) return ELSA_ERR_SHAPE;
+  if (finalize ? !y : (!m_out || !S_out || !W_out)) return ELSA_ERR_SHAPE;
+  if (rows == 0) return ELSA_OK;
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  MergeParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  mp.m = m;
+  mp.S = S;
+  mp.W = W;
+  mp.parts = parts;
+  mp.rows = rows;
+  mp.dv = dv;
+  mp.w_pitch = dv;
+  mp.part_stride = part_stride;
+  mp.log2_domain = 0;
+  mp.finalize = finalize ? 1 : 0;
+  mp.y = y;
+  mp.n_q = 0;  // dense [rows][dv] output
+  mp.m_out = m_out;
+  mp.S_out = S_out;
+  mp.W_out = W_out;
+  mp.out_pitch = dv;
+  mp.err = dc->err;
+  return launch_merge(mp, static_cast<cudaStream_t>(stream));
+}
+
+int elsa_get_device_error(void* stream, int* code) {
+  if (!code) return ELSA_ERR_SHAPE;
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  cudaStream_t strm = static_cast<cudaStream_t>(stream);
+  int host = 0;
+  if (cudaMemcpyAsync(&host, dc->err, sizeof(int), cudaMemcpyDeviceToHost, strm) != cudaSuccess)
+    return ELSA_ERR_CUDA;
+  if (cudaMemsetAsync(dc->err, 0, sizeof(int), strm) != cudaSuccess) return ELSA_ERR_CUDA;
+  if (cudaStreamSynchronize(strm) != cudaSuccess) return ELSA_ERR_CUDA;
+  *code = host;
+  return ELSA_OK;
+}
+
+int elsa_ffma_peak(void* stream, double* tflops) {
+  if (!tflops) return ELSA_ERR_SHAPE;
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  cudaStream_t strm = static_cast<cudaStream_t>(stream);
+  float* sink = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&sink), 256 * sizeof(float), strm) != cudaSuccess)
+    return ELSA_ERR_CUDA;
+  const int blocks = dc->sms * 4;
+  const int threads = 256;
+  const int iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  ffma_peak_kernel<<<blocks, threads, 0, strm>>>(sink, iters / 4, 0.5f);  // warm-up
+  cudaEventRecord(e0, strm);
+  ffma_peak_kernel<<<blocks, threads, 0, strm>>>(sink, iters, 0.5f);
+  cudaEventRecord(e1, strm);
+  int rc = ELSA_OK;
+  if (cudaEventSynchronize(e1) != cudaSuccess) rc = ELSA_ERR_CUDA;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeAsync(sink, strm);
+  if (rc) return rc;
+  const double flops = 2.0 * double(kFfmaPerIter) * iters * double(blocks) * threads;
+  *tflops = flops / (double(ms) * 1e-3) / 1e12;
+  return ELSA_OK;
+}
+
+int elsa_last_launch_count(void) { return t_last_launches; }
+
+}  // extern "C"
