@@ -289,7 +289,13 @@ void fill_common(FwdParams& p, const float* q, const float* k, const float* v,
   p.vs_b = v_st[0];
   p.vs_h = v_st[1];
   p.vs_r = v_st[2];
-  p.c = float(scale * kLog2e);
+  // exponents are evaluated as exp2(acc * c - m) with c > 0; a negative scale
+  // is folded into Q^T inside the kernel, a zero scale becomes a uniform
+  // softmax through a vanishing positive c
+  double c = std::fabs(scale) * kLog2e;
+  if (c < 1e-30) c = 1e-30;
+  p.c = float(c);
+  p.neg = scale < 0 ? 1 : 0;
 }
 
 size_t split_ws_bytes(const elsa_shape* s, int splits) {

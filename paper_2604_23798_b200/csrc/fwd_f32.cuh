@@ -57,7 +57,8 @@ struct FwdParams {
   int64_t ks_b, ks_h, ks_r;
   int64_t vs_b, vs_h, vs_r;
   int64_t ys_b, ys_h, ys_r;
-  float c;  // scale * log2(e)
+  float c;    // |scale| * log2(e)
+  int neg;    // scale < 0: fold the sign into Q^T
   int kv_begin, kv_end;
   int tiles_per_split;
   int qtiles;
@@ -80,40 +81,42 @@ struct FwdTraits {
   static constexpr int D = 64;
   static constexpr int DV = 64;
   static constexpr int TQ = 16 * W;
-  static constexpr int QP = D + 4;    // Q/K smem pitch in floats (272 B)
-  static constexpr int VP = DV;       // V smem pitch
-  static constexpr int PP = TK + 16;  // P pitch, == 16 (mod 32) floats
+  static constexpr int QP = D + 4;    // raw Q / K row pitch in floats (272 B; TMA box width)
+  static constexpr int QTP = TQ;      // Q^T pitch: Qt[d][row position]
+  static constexpr int VP = DV;       // V row pitch
+  static constexpr int PTP = 20;      // P^T pitch: Pt[key][row position], 16 rows + 4 pad
   static constexpr int RK = TK / 16;  // keys per lane in GEMM1
-  static constexpr int Q_FLOATS = TQ * QP;
+  static constexpr int QT_FLOATS = D * QTP;
   static constexpr int K_FLOATS = TK * QP;
   static constexpr int V_FLOATS = TK * VP;
-  static constexpr int P_FLOATS = W * 16 * PP;
+  static constexpr int P_FLOATS = W * TK * PTP;  // also the raw-Q TMA landing zone
+  static constexpr int QRAW_FLOATS = TQ * QP;
   static constexpr int THREADS = (W + 1) * 32;
   static constexpr size_t BAR_OFFSET =
-      size_t(Q_FLOATS + STAGES * (K_FLOATS + V_FLOATS) + P_FLOATS) * 4;
+      size_t(QT_FLOATS + STAGES * (K_FLOATS + V_FLOATS) + P_FLOATS) * 4;
   static constexpr size_t SMEM_BYTES = BAR_OFFSET + (2 * STAGES + 1) * 8;
   static constexpr uint32_t KV_TX_BYTES = uint32_t(K_FLOATS + V_FLOATS) * 4;
-  static constexpr uint32_t Q_TX_BYTES = uint32_t(Q_FLOATS) * 4;
+  static constexpr uint32_t Q_TX_BYTES = uint32_t(QRAW_FLOATS) * 4;
   static_assert(TK % 16 == 0, "TK must be a multiple of 16");
-  static_assert((PP % 32) == 16, "P pitch must be 16 mod 32");
-  static_assert((Q_FLOATS * 4) % 128 == 0 && (K_FLOATS * 4) % 128 == 0 &&
+  static_assert(QRAW_FLOATS <= P_FLOATS, "raw Q must fit the P area");
+  static_assert((QT_FLOATS * 4) % 128 == 0 && (K_FLOATS * 4) % 128 == 0 &&
                     (V_FLOATS * 4) % 128 == 0,
                 "TMA destinations must stay 128-byte aligned");
 };
 
 template <class T>
-__device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qs, float* Ks,
+__device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw, float* Ks,
                                                  float* Vs, uint64_t* full, uint64_t* empty,
                                                  uint64_t* qbar, int b, int h, int q0,
                                                  int t_begin, int ntiles, int lane) {
   // Plain-load fallback for operands TMA cannot describe (misaligned base or
   // strides, zero strides). Same smem layout as the TMA boxes, zero-filled.
   const float* qg = p.q + int64_t(b) * p.qs_b + int64_t(h) * p.qs_h;
-  for (int idx = lane; idx < T::Q_FLOATS; idx += 32) {
+  for (int idx = lane; idx < T::QRAW_FLOATS; idx += 32) {
     const int r = idx / T::QP, c = idx - r * T::QP;
     float val = 0.f;
     if (c < p.d && q0 + r < p.n_q) val = qg[int64_t(q0 + r) * p.qs_r + c];
-    Qs[idx] = val;
+    Qraw[idx] = val;
   }
   __threadfence_block();
   __syncwarp();
@@ -144,19 +147,24 @@ __device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qs, 
   }
 }
 
+__device__ __forceinline__ float f4(const float4& v, int c) {
+  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+}
+
 template <int W_, int TK_, int STAGES_, bool kTMA>
 __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
     fwd_f32_kernel(const __grid_constant__ FwdParams p, const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV) {
   using T = FwdTraits<W_, TK_, STAGES_>;
-  constexpr int TK = T::TK, QP = T::QP, VP = T::VP, PP = T::PP, RK = T::RK;
+  constexpr int TK = T::TK, QP = T::QP, QTP = T::QTP, VP = T::VP, PTP = T::PTP, RK = T::RK;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  float* Qs = reinterpret_cast<float*>(smem_raw);
-  float* Ks = Qs + T::Q_FLOATS;
+  float* Qt = reinterpret_cast<float*>(smem_raw);
+  float* Ks = Qt + T::QT_FLOATS;
   float* Vs = Ks + T::STAGES * T::K_FLOATS;
   float* Ps = Vs + T::STAGES * T::V_FLOATS;
+  float* Qraw = Ps;  // raw Q lands in the P area and is transposed out before first use of P
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + T::BAR_OFFSET);
   uint64_t* empty = full + T::STAGES;
   uint64_t* qbar = empty + T::STAGES;
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
         ptx::prefetch_tmap(&tmK);
         ptx::prefetch_tmap(&tmV);
         ptx::mbar_arrive_expect_tx(qbar, T::Q_TX_BYTES);
-        ptx::tma_load_4d(Qs, &tmQ, qbar, 0, q0, h, b);
+        ptx::tma_load_4d(Qraw, &tmQ, qbar, 0, q0, h, b);
         for (int t = 0; t < ntiles; ++t) {
           const int s = t % T::STAGES;
           if (t >= T::STAGES) ptx::mbar_wait(&empty[s], ((t / T::STAGES) - 1) & 1);
@@ -206,29 +214,62 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
         }
       }
     } else {
-      producer_generic<T>(p, Qs, Ks, Vs, full, empty, qbar, b, h, q0, t_begin, ntiles, lane);
+      producer_generic<T>(p, Qraw, Ks, Vs, full, empty, qbar, b, h, q0, t_begin, ntiles, lane);
     }
     return;
   }
 
   // ---------------- consumer warps ----------------
-  const int rg = lane >> 4;  // row group: rows rg + 2i
-  const int g = lane & 15;   // key group (GEMM1) / column group (GEMM2)
-  const float* qb = Qs + (warp * 16 + rg) * QP;
-  float* pw = Ps + warp * 16 * PP;
-  float* pwr = pw + rg * PP;  // this lane's row base in P (rows rg + 2i)
+  // lane = 16*h + 8*rg + k8: each half-warp holds both row groups and 8 of
+  // the 16 key/column groups, so every LDS.128 touches <= 128 B per half-warp
+  // (one shared-memory wavefront per half)
+  const int rg = (lane >> 3) & 1;               // row group: rows rg + 2i
+  const int g = ((lane >> 4) << 3) | (lane & 7);  // key group (GEMM1) / column group (GEMM2)
 
-  float o[8][4];
-  float mrow[8], lrow[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    mrow[i] = -CUDART_INF_F;
-    lrow[i] = 0.f;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) o[i][c] = 0.f;
-  }
-
+  // Q^T, once per CTA: each warp transposes its own 16 rows out of the raw TMA
+  // box into Qt[d][pos], pos = 16*warp + 8*(r & 1) + (r >> 1) for local row r,
+  // so a lane's 8 rows (rg + 2i) are 8 consecutive floats: two LDS.128 per d.
+  // The sign of a negative scale is folded in here (x = (-q).k * |c|).
   ptx::mbar_wait(qbar, 0);
+  {
+    const int r = lane & 15;
+    const int dh = (lane >> 4) * 32;
+    const float* src = Qraw + (warp * 16 + r) * QP + dh;
+    float* dst = Qt + (warp * 16 + 8 * (r & 1) + (r >> 1)) + dh * QTP;
+    const float sgn = p.neg ? -1.f : 1.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 v = ptx::lds128(src + 4 * c);
+      dst[(4 * c + 0) * QTP] = v.x * sgn;
+      dst[(4 * c + 1) * QTP] = v.y * sgn;
+      dst[(4 * c + 2) * QTP] = v.z * sgn;
+      dst[(4 * c + 3) * QTP] = v.w * sgn;
+    }
+  }
+  // every consumer warp must finish reading raw Q before any warp writes P over it
+  asm volatile("bar.sync 1, %0;" ::"r"(T::W * 32) : "memory");
+
+  const float* qt = Qt + warp * 16 + rg * 8;
+  float* pw = Ps + warp * TK * PTP;
+  const float* ptr = pw + rg * 8;
+  const float c2 = p.c;  // |scale| * log2(e) > 0
+  using ptx::f32x2;
+  const f32x2 cc = ptx::pack2(c2, c2);
+
+  // Row pairs: lane rows (rg + 2i), i = 0..7, are held as 4 packed pairs
+  // ip = (i = 2ip, 2ip+1) so every GEMM FMA is an FFMA2 outer-product step
+  // (one broadcast scalar x one row pair), two FP32 FMAs per issue slot.
+  f32x2 o2[4][4];    // W accumulator: [row pair][column 4g + c]
+  float mrow[8];     // running anchors (log2 units)
+  f32x2 l2[4];       // running normalizer partials (this lane's keys)
+#pragma unroll
+  for (int ip = 0; ip < 4; ++ip) {
+    l2[ip] = 0ull;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o2[ip][c] = 0ull;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mrow[i] = -CUDART_INF_F;
 
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % T::STAGES;
@@ -236,99 +277,130 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
     const float* ks = Ks + s * T::K_FLOATS + g * QP;
     const float* vs = Vs + s * T::V_FLOATS + 4 * g;
 
-    // ---- GEMM1: S = Q K^T over the 64-wide head dim (FP32 FFMA) ----
-    float sc[8][RK];
+    // ---- GEMM1: S = Q K^T on FFMA2: s2[ip][j] += k_j[d] (bcast) * Qt[d][row pair ip]
+    f32x2 s2[4][RK];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int ip = 0; ip < 4; ++ip)
 #pragma unroll
-      for (int j = 0; j < RK; ++j) sc[i][j] = 0.f;
+      for (int j = 0; j < RK; ++j) s2[ip][j] = 0ull;
 
-#pragma unroll 4
+#pragma unroll 1
     for (int c = 0; c < T::D / 4; ++c) {
       float4 kf[RK];
 #pragma unroll
       for (int j = 0; j < RK; ++j) kf[j] = ptx::lds128(ks + j * 16 * QP + 4 * c);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 qf = ptx::lds128(qb + i * 2 * QP + 4 * c);
+      for (int dd = 0; dd < 4; ++dd) {
+        f32x2 q2[4];
+        ptx::lds128x2(qt + (4 * c + dd) * QTP, q2[0], q2[1]);
+        ptx::lds128x2(qt + (4 * c + dd) * QTP + 4, q2[2], q2[3]);
 #pragma unroll
         for (int j = 0; j < RK; ++j) {
-          sc[i][j] = fmaf(qf.x, kf[j].x, sc[i][j]);
-          sc[i][j] = fmaf(qf.y, kf[j].y, sc[i][j]);
-          sc[i][j] = fmaf(qf.z, kf[j].z, sc[i][j]);
-          sc[i][j] = fmaf(qf.w, kf[j].w, sc[i][j]);
+          const float kv = f4(kf[j], dd);
+          const f32x2 kb = ptx::pack2(kv, kv);
+          // snake order keeps one operand in the reuse cache across the switch
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ip = (j & 1) ? 3 - u : u;
+            ptx::ffma2(s2[ip][j], kb, q2[ip]);
+          }
         }
       }
     }
 
-    // ---- leaf anchors in log2 units; mask keys past this split's range ----
+    // ---- mask keys past this split's range ----
     const int key0 = p.kv_begin + (t_begin + t) * TK;
-    const bool ragged = key0 + TK > kv_hi;
+    if (key0 + TK > kv_hi) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < RK; ++j)
+        if (key0 + g + 16 * j >= kv_hi) {
+          const f32x2 ninf = ptx::pack2(-CUDART_INF_F, -CUDART_INF_F);
 #pragma unroll
-      for (int j = 0; j < RK; ++j) {
-        float x = sc[i][j] * p.c;
-        if (ragged && key0 + g + 16 * j >= kv_hi) x = -CUDART_INF_F;
-        sc[i][j] = x;
-      }
+          for (int ip = 0; ip < 4; ++ip) s2[ip][j] = ninf;
+        }
+    }
 
-    // ---- tile state (m_t, S_t) and the monoid combine into the running row state ----
+    // ---- tile state (m_t, S_t) and the monoid combine into the running row state.
+    // Anchors in log2 units: m = fl(max_j acc_j * c). Each exponent is one FMA
+    // acc*c - m (exact product, one rounding), so near-max keys carry an
+    // absolute exponent error ~u*|s - m| rather than ~u*|s|.
+    f32x2 mneg2[4], corr2[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float mx = sc[i][0];
+    for (int ip = 0; ip < 4; ++ip) {
+      float mlo = ptx::lo2(s2[ip][0]), mhi = ptx::hi2(s2[ip][0]);
 #pragma unroll
-      for (int j = 1; j < RK; ++j) mx = fmaxf(mx, sc[i][j]);
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-      const float mnew = fmaxf(mrow[i], mx);
+      for (int j = 1; j < RK; ++j) {
+        mlo = fmaxf(mlo, ptx::lo2(s2[ip][j]));
+        mhi = fmaxf(mhi, ptx::hi2(s2[ip][j]));
+      }
+#pragma unroll
+      for (int sh = 1; sh <= 16; sh <<= 1) {
+        if (sh == 8) continue;  // lane bit 3 is the row group
+        mlo = fmaxf(mlo, __shfl_xor_sync(0xffffffffu, mlo, sh));
+        mhi = fmaxf(mhi, __shfl_xor_sync(0xffffffffu, mhi, sh));
+      }
+      const float nlo = fmaxf(mrow[2 * ip], mlo * c2);
+      const float nhi = fmaxf(mrow[2 * ip + 1], mhi * c2);
       // running side's factor; exp2(-inf) = 0 for the identity start state
-      const float corr = ptx::ex2(mrow[i] - mnew);
-      float ps = 0.f;
+      corr2[ip] = ptx::pack2(ptx::ex2(mrow[2 * ip] - nlo), ptx::ex2(mrow[2 * ip + 1] - nhi));
+      mrow[2 * ip] = nlo;
+      mrow[2 * ip + 1] = nhi;
+      mneg2[ip] = ptx::pack2(-nlo, -nhi);
+    }
+    f32x2 p2[4][RK];
+#pragma unroll
+    for (int ip = 0; ip < 4; ++ip) {
+      f32x2 ps = 0ull;
 #pragma unroll
       for (int j = 0; j < RK; ++j) {
-        const float pv = ptx::ex2(sc[i][j] - mnew);
-        ps += pv;
-        pwr[2 * i * PP + g + 16 * j] = pv;
+        const f32x2 x = ptx::ffma2r(s2[ip][j], cc, mneg2[ip]);
+        float xlo, xhi;
+        ptx::unpack2(x, xlo, xhi);
+        p2[ip][j] = ptx::pack2(ptx::ex2(xlo), ptx::ex2(xhi));
+        ps = j == 0 ? p2[ip][j] : ptx::fadd2(ps, p2[ip][j]);
       }
-      lrow[i] = fmaf(lrow[i], corr, ps);
+      l2[ip] = ptx::ffma2r(l2[ip], corr2[ip], ps);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) o[i][c] *= corr;
-      mrow[i] = mnew;
+      for (int c = 0; c < 4; ++c) o2[ip][c] = ptx::fmul2(o2[ip][c], corr2[ip]);
+    }
+    // P^T: key-major, this lane's 8 rows contiguous -> two STS.128 per key
+#pragma unroll
+    for (int j = 0; j < RK; ++j) {
+      float* dst = pw + (g + 16 * j) * PTP + rg * 8;
+      *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(p2[0][j], p2[1][j]);
+      *reinterpret_cast<ulonglong2*>(dst + 4) = make_ulonglong2(p2[2][j], p2[3][j]);
     }
     __syncwarp();
 
-    // ---- GEMM2: W += P V (FP32 FFMA) ----
+    // ---- GEMM2: W += P V on FFMA2: o2[ip][c] += v_j[c] (bcast) * Pt[j][row pair ip]
 #pragma unroll 4
-    for (int jc = 0; jc < TK / 4; ++jc) {
-      float4 vf[4];
+    for (int jj = 0; jj < TK; ++jj) {
+      f32x2 pr[4];
+      ptx::lds128x2(ptr + jj * PTP, pr[0], pr[1]);
+      ptx::lds128x2(ptr + jj * PTP + 4, pr[2], pr[3]);
+      const float4 vf = ptx::lds128(vs + jj * VP);
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) vf[jj] = ptx::lds128(vs + (4 * jc + jj) * VP);
+      for (int c = 0; c < 4; ++c) {
+        const float vv = f4(vf, c);
+        const f32x2 vb = ptx::pack2(vv, vv);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 pf = ptx::lds128(pwr + 2 * i * PP + 4 * jc);
-        o[i][0] = fmaf(pf.x, vf[0].x, o[i][0]);
-        o[i][1] = fmaf(pf.x, vf[0].y, o[i][1]);
-        o[i][2] = fmaf(pf.x, vf[0].z, o[i][2]);
-        o[i][3] = fmaf(pf.x, vf[0].w, o[i][3]);
-        o[i][0] = fmaf(pf.y, vf[1].x, o[i][0]);
-        o[i][1] = fmaf(pf.y, vf[1].y, o[i][1]);
-        o[i][2] = fmaf(pf.y, vf[1].z, o[i][2]);
-        o[i][3] = fmaf(pf.y, vf[1].w, o[i][3]);
-        o[i][0] = fmaf(pf.z, vf[2].x, o[i][0]);
-        o[i][1] = fmaf(pf.z, vf[2].y, o[i][1]);
-        o[i][2] = fmaf(pf.z, vf[2].z, o[i][2]);
-        o[i][3] = fmaf(pf.z, vf[2].w, o[i][3]);
-        o[i][0] = fmaf(pf.w, vf[3].x, o[i][0]);
-        o[i][1] = fmaf(pf.w, vf[3].y, o[i][1]);
-        o[i][2] = fmaf(pf.w, vf[3].z, o[i][2]);
-        o[i][3] = fmaf(pf.w, vf[3].w, o[i][3]);
+        for (int u = 0; u < 4; ++u) {
+          const int ip = (c & 1) ? 3 - u : u;
+          ptx::ffma2(o2[ip][c], vb, pr[ip]);
+        }
       }
     }
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&empty[s]);
+  }
+
+  // unpack the row-pair state for the epilogue
+  float o[8][4], lrow[8];
+#pragma unroll
+  for (int ip = 0; ip < 4; ++ip) {
+    ptx::unpack2(l2[ip], lrow[2 * ip], lrow[2 * ip + 1]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) ptx::unpack2(o2[ip][c], o[2 * ip][c], o[2 * ip + 1][c]);
   }
 
   // ---------------- epilogue ----------------
@@ -338,7 +410,7 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
     l += __shfl_xor_sync(0xffffffffu, l, 1);
     l += __shfl_xor_sync(0xffffffffu, l, 2);
     l += __shfl_xor_sync(0xffffffffu, l, 4);
-    l += __shfl_xor_sync(0xffffffffu, l, 8);
+    l += __shfl_xor_sync(0xffffffffu, l, 16);
     const int qrow = q0 + warp * 16 + rg + 2 * i;
     if (qrow >= p.n_q) continue;
     if (p.mode == kModeFinal) {

@@ -80,5 +80,55 @@ __device__ __forceinline__ float4 lds128(const float* p) {
   return *reinterpret_cast<const float4*>(p);
 }
 
+// ---- packed FP32x2 (sm_100 FFMA2 / FMUL2 / FADD2), lanes = (lo, hi) ----
+// Each op is two IEEE round-to-nearest FP32 operations; results are
+// bit-identical to the scalar fmaf / __fmul_rn / __fadd_rn on each lane.
+typedef unsigned long long f32x2;
+
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(f32x2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ float lo2(f32x2 v) {
+  float lo, hi;
+  unpack2(v, lo, hi);
+  return lo;
+}
+__device__ __forceinline__ float hi2(f32x2 v) {
+  float lo, hi;
+  unpack2(v, lo, hi);
+  return hi;
+}
+// d = a * b + d; `a` is usually pack2(x, x), which ptxas folds into the
+// FFMA2 broadcast operand form (Rn.F32).
+__device__ __forceinline__ void ffma2(f32x2& d, f32x2 a, f32x2 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ f32x2 ffma2r(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 16-byte shared load as two packed pairs (x, y) and (z, w)
+__device__ __forceinline__ void lds128x2(const float* p, f32x2& a, f32x2& b) {
+  const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(p);
+  a = v.x;
+  b = v.y;
+}
+
 }  // namespace ptx
 }  // namespace elsa
