@@ -334,7 +334,7 @@ def main():
         "k4_ffma_measured": k4, "frac_of_k4": (value / k4) if k4 else None,
         "traffic": traffic, "traffic_workload": traffic_workload,
         "algorithmic_bytes_per_launch": 4 * B * H * (n * 64 * 3 + n * 64),
-        "kernel": "elsa::fwd_f32_kernel<4,64,2,true>",
+        "kernel": "elsa::fwd_f32_kernel (" + elsa.describe_plan(q, k, v) + ")" if world == 1 else "elsa::fwd_f32_kernel",
         "measurement": "CUDA events on the launching stream around the K timed steps; "
                        "one kernel launch per step at this shape",
     }
@@ -365,7 +365,7 @@ def main():
             tf = flops(bb, hh, nn, nn) / (t_ms * 1e-3) / 1e12
             sweep.append({"B": bb, "H": hh, "n": nn, "ms": t_ms, "tflops": tf,
                           "frac_ffma_peak": tf / spec_peak,
-                          "kv_splits": elsa.resolve_kv_splits(qq, kk, vv)})
+                          "plan": elsa.describe_plan(qq, kk, vv)})
             del qq, kk, vv
         # GPU comparator on the same box: torch SDPA FP32 (TF32 off), the paper's ME-SDPA
         try:

@@ -125,6 +125,14 @@ int elsa_ffma_peak(void* stream, double* tflops);
  * host thread launched (for the bench's gpu_launches accounting). */
 int elsa_last_launch_count(void);
 
+/* Human-readable launch plan elsa_fwd_f32 would use for this shape
+ * (kernel configuration, query/key tile sizes, kv split count). */
+int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n);
+
+/* Text of the last CUDA failure reported as ELSA_ERR_CUDA on this host
+ * thread ("" if none). */
+const char* elsa_last_cuda_error(void);
+
 #ifdef __cplusplus
 }
 #endif

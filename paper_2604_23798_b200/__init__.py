@@ -15,6 +15,7 @@ Entry points:
 
 from .attention import (  # noqa: F401
     check_device_error,
+    describe_plan,
     ffma_peak_tflops,
     last_launch_count,
     merge_states,

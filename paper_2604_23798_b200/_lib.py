@@ -16,7 +16,8 @@ from .errors import ElsaCudaError, ElsaLibraryError, NumericalError, ShapeError,
 
 __all__ = ["lib", "ElsaShape", "check_status", "LIB_PATH", "EXPORTED_SYMBOLS"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libelsa.so")
+LIB_PATH = os.environ.get("ELSA_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libelsa.so")  # env override: build A/B experiments
 
 # Every symbol include/elsa.h declares.
 EXPORTED_SYMBOLS = (
@@ -31,6 +32,8 @@ EXPORTED_SYMBOLS = (
     "elsa_get_device_error",
     "elsa_ffma_peak",
     "elsa_last_launch_count",
+    "elsa_last_cuda_error",
+    "elsa_describe_plan",
 )
 
 ABI_VERSION = 1
@@ -92,6 +95,10 @@ def _declare(h):
     h.elsa_ffma_peak.argtypes = [c_vp, ctypes.POINTER(c_dbl)]
     h.elsa_last_launch_count.restype = c_int
     h.elsa_last_launch_count.argtypes = []
+    h.elsa_last_cuda_error.restype = ctypes.c_char_p
+    h.elsa_last_cuda_error.argtypes = []
+    h.elsa_describe_plan.restype = c_int
+    h.elsa_describe_plan.argtypes = [shp, c_int, ctypes.c_char_p, c_sz]
 
 
 def lib():
@@ -132,4 +139,4 @@ def check_status(status, what="elsa"):
         raise NumericalError(msg)
     if status == ELSA_ERR_WORKSPACE:
         raise WorkspaceError(msg)
-    raise ElsaCudaError(msg)
+    raise ElsaCudaError(f"{msg}: {lib().elsa_last_cuda_error().decode()}")

@@ -30,6 +30,7 @@ __all__ = [
     "merge_states",
     "check_device_error",
     "resolve_kv_splits",
+    "describe_plan",
     "ffma_peak_tflops",
 ]
 
@@ -123,6 +124,17 @@ def resolve_kv_splits(q, k, v, kv_splits=0):
     if r < 0:
         _lib.check_status(-r, "elsa_resolve_kv_splits")
     return r
+
+
+def describe_plan(q, k, v, kv_splits=0):
+    """The launch plan (kernel configuration, tiles, kv splits) for these shapes."""
+    q4, k4, v4 = _as_4d(q, "query"), _as_4d(k, "key"), _as_4d(v, "value")
+    shp = _shape(q4, k4, v4)
+    buf = ctypes.create_string_buffer(128)
+    with torch.cuda.device(q4.device):
+        _lib.check_status(_lib.lib().elsa_describe_plan(ctypes.byref(shp), int(kv_splits), buf, 128),
+                          "elsa_describe_plan")
+    return buf.value.decode()
 
 
 def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.0,

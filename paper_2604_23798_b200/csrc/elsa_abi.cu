@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -34,6 +35,26 @@ constexpr int kMaxSplits = kMergeMaxParts;
 constexpr double kLog2e = 1.4426950408889634074;
 
 thread_local int t_last_launches = 0;
+thread_local char t_last_cuda_error[256] = "";
+
+#ifdef ELSA_TRACE
+unsigned long long* g_trace = nullptr;
+unsigned long long* trace_buffer() {
+  if (!g_trace) {
+    cudaMalloc(&g_trace, sizeof(unsigned long long) * kTraceCtas * 16 * kTraceTiles * kTracePoints);
+    cudaMemset(g_trace, 0, sizeof(unsigned long long) * kTraceCtas * 16 * kTraceTiles * kTracePoints);
+  }
+  return g_trace;
+}
+#else
+unsigned long long* trace_buffer() { return nullptr; }
+#endif
+
+int cuda_fail(cudaError_t e, const char* where) {
+  std::snprintf(t_last_cuda_error, sizeof(t_last_cuda_error), "%s: %s (%d)", where,
+                cudaGetErrorString(e), int(e));
+  return ELSA_ERR_CUDA;
+}
 
 struct DeviceCache {
   bool ready = false;
@@ -77,32 +98,38 @@ int current_device_cache(DeviceCache** out) {
 }
 
 // ---------------------------------------------------------------------------
-// Forward kernel configurations. Selected by ELSA_FWD_CFG (benchmarking aid);
-// the default is the measured best.
+// Forward kernel configurations. The planner picks one per shape (see
+// plan_for); ELSA_FWD_CFG forces one (benchmarking aid).
+//   w4r8 : 4 consumer warps x 16 rows (TQ = 64),  2 CTAs / SM, 8 rows per lane
+//   w8r8 : 8 consumer warps x 16 rows (TQ = 128), 1 CTA / SM
+//   w8r16: 8 consumer warps x 32 rows (TQ = 256), 1 CTA / SM, 16 rows per
+//          lane (setmaxnreg register split with a producer warpgroup)
 // ---------------------------------------------------------------------------
-enum CfgId { kCfgW4S2 = 0, kCfgW8S2 = 1, kCfgW8S3 = 2, kCfgCount = 3 };
+enum CfgId { kCfgW4R8 = 0, kCfgW8R16 = 1, kCfgW8R8 = 2, kCfgCount = 3, kCfgAuto = -1 };
 
-int active_cfg() {
+int forced_cfg() {
   static int cfg = [] {
     const char* e = std::getenv("ELSA_FWD_CFG");
-    if (e && !std::strcmp(e, "w8s2")) return int(kCfgW8S2);
-    if (e && !std::strcmp(e, "w8s3")) return int(kCfgW8S3);
-    return int(kCfgW4S2);
+    if (e && !std::strcmp(e, "w4r8")) return int(kCfgW4R8);
+    if (e && !std::strcmp(e, "w8r8")) return int(kCfgW8R8);
+    if (e && !std::strcmp(e, "w8r16")) return int(kCfgW8R16);
+    return int(kCfgAuto);
   }();
   return cfg;
 }
 
 struct CfgInfo {
   int tq, tk, ctas_per_sm;
+  double eff;  // measured relative per-SM throughput at n = 16K
 };
 CfgInfo cfg_info(int cfg) {
   switch (cfg) {
-    case kCfgW8S2:
-      return {128, 64, 1};
-    case kCfgW8S3:
-      return {128, 64, 1};
+    case kCfgW8R16:
+      return {256, 64, 1, 1.02};
+    case kCfgW8R8:
+      return {128, 64, 1, 0.99};
     default:
-      return {64, 64, 2};
+      return {64, 64, 2, 1.0};
   }
 }
 
@@ -121,52 +148,71 @@ bool valid_shape(const elsa_shape* s) {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Split plan. Cost model in units of one key tile of one CTA:
-//   waves(s) * (ceil(tiles / s) + kCtaOverheadTiles)            forward kernel
-// + [s > 1] * (1 + s * rows * 264 B / kBytesPerTile)            partial-state round trip + merge
-// minimised over s <= min(tiles, 32), with s >= ceil(tiles / kMaxChainTiles) so
-// no CTA folds more than kMaxChainTiles tiles sequentially (bounded chain
-// depth; the rest of the reduction is the log-depth split tree).
+// Launch plan (config + kv split count). Cost model in units of one
+// 64-row x 64-key tile on a whole SM:
+//   waves(cfg, s) * (ceil(tiles / s) + kCtaOverheadTiles) * (TQ / 64) * ctas_per_sm / eff
+// + [s > 1] * (1 + s * rows * kSplitUnitsPerRow)     partial-state round trip + merge pass
+// minimised over the configs and s <= min(tiles, 32), with
+// s >= ceil(tiles / kMaxChainTiles) so no CTA folds more than kMaxChainTiles
+// tiles sequentially (bounded chain depth; the rest is the log-depth tree).
 constexpr double kCtaOverheadTiles = 2.0;
-constexpr double kBytesPerTile = 3.0e7;
+constexpr double kSplitUnitsPerRow = 3.4e-5;  // 528 B/row at ~5 TB/s over a ~3.1 us unit
 constexpr int64_t kMaxChainTiles = 256;
 
-int plan_splits(int64_t ctas, int64_t tiles, int64_t rows, int64_t slots, int requested) {
-  if (tiles < 1) return 1;
-  int64_t s = 1;
-  if (requested > 0) {
-    s = requested;
-  } else {
-    const int64_t smax = tiles < kMaxSplits ? tiles : kMaxSplits;
-    int64_t smin = ceil_div(tiles, kMaxChainTiles);
-    if (smin > smax) smin = smax;
-    double best = 1e300;
-    for (int64_t cand = smin; cand <= smax; ++cand) {
-      double t = double(ceil_div(ctas * cand, slots)) *
-                 (double(ceil_div(tiles, cand)) + kCtaOverheadTiles);
-      if (cand > 1) t += 1.0 + double(cand) * double(rows) * 264.0 / kBytesPerTile;
-      if (t < best - 1e-9) {
-        best = t;
-        s = cand;
-      }
-    }
-  }
+struct Plan {
+  int cfg;
+  int splits;
+};
+
+double plan_cost(const CfgInfo& ci, int64_t ctas, int64_t tiles, int64_t rows, int64_t sms,
+                 int64_t s) {
+  const int64_t slots = sms * ci.ctas_per_sm;
+  double t = double(ceil_div(ctas * s, slots)) *
+             (double(ceil_div(tiles, s)) + kCtaOverheadTiles) * (ci.tq / 64.0) *
+             ci.ctas_per_sm / ci.eff;
+  if (s > 1) t += 1.0 + double(s) * double(rows) * kSplitUnitsPerRow;
+  return t;
+}
+
+int64_t normalize_splits(int64_t s, int64_t tiles) {
   if (s > tiles) s = tiles;
   if (s > kMaxSplits) s = kMaxSplits;
   if (s < 1) s = 1;
   // drop empty splits: the effective count is ceil(tiles / tiles_per_split)
   const int64_t tps = ceil_div(tiles, s);
-  return int(ceil_div(tiles, tps));
+  return ceil_div(tiles, tps);
 }
 
-int resolve_splits_for(const elsa_shape* s, int64_t kv_len, int requested, int sms) {
-  const CfgInfo ci = cfg_info(active_cfg());
-  const int64_t qtiles = ceil_div(s->n_q, ci.tq);
-  const int64_t ctas = qtiles * s->B * s->H;
-  const int64_t tiles = ceil_div(kv_len, ci.tk);
-  if (ctas == 0) return 1;
-  const int64_t rows = s->B * s->H * s->n_q;
-  return plan_splits(ctas, tiles, rows, int64_t(sms) * ci.ctas_per_sm, requested);
+Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms) {
+  Plan best{kCfgW4R8, 1};
+  double best_t = 1e300;
+  const int forced = forced_cfg();
+  for (int cfg = 0; cfg < kCfgCount; ++cfg) {
+    if (forced != kCfgAuto && cfg != forced) continue;
+    if (forced == kCfgAuto && cfg == kCfgW8R8) continue;  // never better than the other two
+    const CfgInfo ci = cfg_info(cfg);
+    const int64_t ctas = ceil_div(sh->n_q, ci.tq) * sh->B * sh->H;
+    const int64_t tiles = ceil_div(kv_len, ci.tk);
+    const int64_t rows = sh->B * sh->H * sh->n_q;
+    if (ctas == 0 || tiles < 1) return Plan{forced == kCfgAuto ? int(kCfgW4R8) : forced, 1};
+    int64_t lo, hi;
+    if (requested > 0) {
+      lo = hi = normalize_splits(requested, tiles);
+    } else {
+      hi = tiles < kMaxSplits ? tiles : kMaxSplits;
+      lo = ceil_div(tiles, kMaxChainTiles);
+      if (lo > hi) lo = hi;
+    }
+    for (int64_t s = lo; s <= hi; ++s) {
+      const int64_t sn = normalize_splits(s, tiles);
+      const double t = plan_cost(ci, ctas, tiles, rows, sms, sn);
+      if (t < best_t - 1e-9) {
+        best_t = t;
+        best = Plan{cfg, int(sn)};
+      }
+    }
+  }
+  return best;
 }
 
 // Sanitise the stride of size-1 axes (any value is semantically irrelevant
@@ -201,11 +247,11 @@ bool encode_map(CUtensorMap* map, const float* base, int64_t inner, int64_t rows
   return r == CUDA_SUCCESS;
 }
 
-template <int W, int TK, int ST>
+template <int W, int TK, int ST, int R>
 int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[3],
                    int64_t v_st[3], int splits, int cfg_slot, DeviceCache* dc,
                    cudaStream_t stream) {
-  using T = FwdTraits<W, TK, ST>;
+  using T = FwdTraits<W, TK, ST, R>;
   p.qtiles = int(ceil_div(s->n_q, T::TQ));
   const int64_t tiles = ceil_div(int64_t(p.kv_end) - p.kv_begin, TK);
   p.tiles_per_split = int(ceil_div(tiles, splits));
@@ -221,35 +267,33 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
   static const bool force_generic = std::getenv("ELSA_FORCE_GENERIC_LOAD") != nullptr;
   if (force_generic) use_tma = false;
 
-  auto kern = use_tma ? fwd_f32_kernel<W, TK, ST, true> : fwd_f32_kernel<W, TK, ST, false>;
+  auto kern = use_tma ? fwd_f32_kernel<W, TK, ST, R, true> : fwd_f32_kernel<W, TK, ST, R, false>;
   const int slot = cfg_slot * 2 + (use_tma ? 1 : 0);
   if (!dc->attr[slot]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(T::SMEM_BYTES)) != cudaSuccess)
-      return ELSA_ERR_CUDA;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(T::SMEM_BYTES));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fwd)");
     dc->attr[slot] = true;
   }
   const int64_t gx = int64_t(p.qtiles) * s->B * s->H;
   if (gx >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
   const dim3 grid{unsigned(gx), unsigned(splits), 1u};
   kern<<<grid, T::THREADS, T::SMEM_BYTES, stream>>>(p, maps[0], maps[1], maps[2]);
-  if (cudaPeekAtLastError() != cudaSuccess) {
-    cudaGetLastError();
-    return ELSA_ERR_CUDA;
-  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "fwd launch");
   ++t_last_launches;
   return ELSA_OK;
 }
 
 int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[3],
-               int64_t v_st[3], int splits, DeviceCache* dc, cudaStream_t stream) {
-  switch (active_cfg()) {
-    case kCfgW8S2:
-      return launch_fwd_cfg<8, 64, 2>(p, s, q_st, k_st, v_st, splits, kCfgW8S2, dc, stream);
-    case kCfgW8S3:
-      return launch_fwd_cfg<8, 64, 3>(p, s, q_st, k_st, v_st, splits, kCfgW8S3, dc, stream);
+               int64_t v_st[3], const Plan& plan, DeviceCache* dc, cudaStream_t stream) {
+  const int splits = plan.splits;
+  switch (plan.cfg) {
+    case kCfgW8R16:
+      return launch_fwd_cfg<8, 64, 2, 16>(p, s, q_st, k_st, v_st, splits, kCfgW8R16, dc, stream);
+    case kCfgW8R8:
+      return launch_fwd_cfg<8, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, kCfgW8R8, dc, stream);
     default:
-      return launch_fwd_cfg<4, 64, 2>(p, s, q_st, k_st, v_st, splits, kCfgW4S2, dc, stream);
+      return launch_fwd_cfg<4, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, kCfgW4R8, dc, stream);
   }
 }
 
@@ -259,10 +303,7 @@ int launch_merge(MergeParams& mp, cudaStream_t stream) {
   const int64_t blocks = ceil_div(mp.rows, kWarps);
   if (blocks >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
   merge_f32_kernel<<<unsigned(blocks), kWarps * 32, 0, stream>>>(mp);
-  if (cudaPeekAtLastError() != cudaSuccess) {
-    cudaGetLastError();
-    return ELSA_ERR_CUDA;
-  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "merge launch");
   ++t_last_launches;
   return ELSA_OK;
 }
@@ -296,6 +337,7 @@ void fill_common(FwdParams& p, const float* q, const float* k, const float* v,
   if (c < 1e-30) c = 1e-30;
   p.c = float(c);
   p.neg = scale < 0 ? 1 : 0;
+  p.trace = trace_buffer();
 }
 
 size_t split_ws_bytes(const elsa_shape* s, int splits) {
@@ -346,7 +388,7 @@ int elsa_resolve_kv_splits(const elsa_shape* shp, int requested) {
   DeviceCache* dc = nullptr;
   int sms = 148;
   if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
-  return resolve_splits_for(shp, shp->n_kv, requested, sms);
+  return plan_for(shp, shp->n_kv, requested, sms).splits;
 }
 
 size_t elsa_workspace_bytes(const elsa_shape* shp, int kv_splits) {
@@ -375,7 +417,8 @@ int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
   sanitize(k_st, shp->n_kv, shp->H, shp->B, shp->d);
   sanitize(v_st, shp->n_kv, shp->H, shp->B, shp->dv);
 
-  const int splits = resolve_splits_for(shp, shp->n_kv, kv_splits, dc->sms);
+  const Plan plan = plan_for(shp, shp->n_kv, kv_splits, dc->sms);
+  const int splits = plan.splits;
   FwdParams p;
   fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
   p.kv_begin = 0;
@@ -390,7 +433,7 @@ int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
 
   if (splits <= 1) {
     p.mode = kModeFinal;
-    return launch_fwd(p, shp, q_st, k_st, v_st, 1, dc, strm);
+    return launch_fwd(p, shp, q_st, k_st, v_st, plan, dc, strm);
   }
   const size_t need = split_ws_bytes(shp, splits);
   if (!workspace || ws_bytes < need) return ELSA_ERR_WORKSPACE;
@@ -403,7 +446,7 @@ int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
   p.part_stride = rows;
   p.pw_pitch = 64;
   p.pw_vec = 1;
-  if (int st = launch_fwd(p, shp, q_st, k_st, v_st, splits, dc, strm)) return st;
+  if (int st = launch_fwd(p, shp, q_st, k_st, v_st, plan, dc, strm)) return st;
 
   MergeParams mp;
   std::memset(&mp, 0, sizeof(mp));
@@ -449,7 +492,8 @@ int elsa_partial_f32(const float* q, const float* k, const float* v, const elsa_
   sanitize(v_st, shp->n_kv, shp->H, shp->B, shp->dv);
 
   const int64_t len = kv_end - kv_begin;
-  int splits = len == 0 ? 1 : resolve_splits_for(shp, len, kv_splits, dc->sms);
+  const Plan plan = len == 0 ? Plan{kCfgW4R8, 1} : plan_for(shp, len, kv_splits, dc->sms);
+  const int splits = plan.splits;
   FwdParams p;
   fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
   p.kv_begin = int(kv_begin);
@@ -463,7 +507,7 @@ int elsa_partial_f32(const float* q, const float* k, const float* v, const elsa_
     p.part_stride = rows;
     p.pw_pitch = int(shp->dv);
     p.pw_vec = (reinterpret_cast<uintptr_t>(W) % 16 == 0) && (shp->dv % 4 == 0);
-    return launch_fwd(p, shp, q_st, k_st, v_st, 1, dc, strm);
+    return launch_fwd(p, shp, q_st, k_st, v_st, plan, dc, strm);
   }
   const size_t need = split_ws_bytes(shp, splits);
   if (!workspace || ws_bytes < need) return ELSA_ERR_WORKSPACE;
@@ -475,7 +519,7 @@ int elsa_partial_f32(const float* q, const float* k, const float* v, const elsa_
   p.part_stride = rows;
   p.pw_pitch = 64;
   p.pw_vec = 1;
-  if (int st = launch_fwd(p, shp, q_st, k_st, v_st, splits, dc, strm)) return st;
+  if (int st = launch_fwd(p, shp, q_st, k_st, v_st, plan, dc, strm)) return st;
   MergeParams mp;
   std::memset(&mp, 0, sizeof(mp));
   mp.m = p.pm;
@@ -576,5 +620,37 @@ int elsa_ffma_peak(void* stream, double* tflops) {
 }
 
 int elsa_last_launch_count(void) { return t_last_launches; }
+
+const char* elsa_last_cuda_error(void) { return t_last_cuda_error; }
+
+int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n) {
+  if (!valid_shape(shp) || kv_splits < 0 || !buf || n == 0) return ELSA_ERR_SHAPE;
+  DeviceCache* dc = nullptr;
+  int sms = 148;
+  if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
+  const Plan pl = plan_for(shp, shp->n_kv, kv_splits, sms);
+  static const char* names[] = {"w4r8", "w8r16", "w8r8"};
+  const CfgInfo ci = cfg_info(pl.cfg);
+  std::snprintf(buf, n, "%s tq=%d tk=%d kv_splits=%d", names[pl.cfg], ci.tq, ci.tk, pl.splits);
+  return ELSA_OK;
+}
+
+// Development aid (ELSA_TRACE builds only; not part of include/elsa.h):
+// copies the phase-timestamp buffer to host memory `out` (n entries).
+int elsa_dev_read_trace(unsigned long long* out, size_t n) {
+#ifdef ELSA_TRACE
+  if (!g_trace) return ELSA_ERR_SHAPE;
+  const size_t total = size_t(kTraceCtas) * 16 * kTraceTiles * kTracePoints;
+  if (n > total) n = total;
+  return cudaMemcpy(out, g_trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+                 cudaSuccess
+             ? ELSA_OK
+             : ELSA_ERR_CUDA;
+#else
+  (void)out;
+  (void)n;
+  return ELSA_ERR_SHAPE;
+#endif
+}
 
 }  // extern "C"

@@ -1,5 +1,5 @@
 // fwd_f32.cuh — K1: the ELSA score-tile producer + per-tile (m,S,W) combine +
-// P.V accumulation + output epilogue, strict FP32 on the FFMA pipe (no tensor
+// P.V accumulation + output epilogue, strict FP32 on the FMA pipe (no tensor
 // cores, no TF32: SPEC.md:343).
 //
 // Reference path this replaces (scanattn, /root/reference/pkg/src/scanattn):
@@ -9,28 +9,34 @@
 //   epilogue Y = W / S, normalizer check          engine.py:375-382
 //   combine arithmetic                            monoid.py:160-200
 //
-// B200 design: the leaf is a whole key tile, not a key.
-// For a 64-key tile each query row's tile state is formed directly in the
+// B200 design: the leaf is a whole key tile, not a key. For a
+// TK-key tile each query row's tile state is formed directly in the
 // un-sum-renorm form of Eq. 5: m_t = rowmax(s) by a 16-lane
-// shuffle butterfly, S_t = sum 2^(s - m_t), W_t = P_t V_t on the FFMA pipe,
-// and folded into the running state with the monoid combine
-// (m, S, W) (+) (m_t, S_t, W_t). Scores live in the log2 domain
-// (x = s * log2(e)) so every exponential is one MUFU.EX2.
+// shuffle butterfly, S_t = sum 2^(s - m_t), W_t = P_t V_t, and folded into the
+// running state with the monoid combine (m,S,W) (+) (m_t,S_t,W_t). Scores live
+// in log2 units so every exponential is one MUFU.EX2.
 //
-// CTA = W consumer warps + 1 TMA producer warp. Each consumer warp owns 16
+// CTA = W consumer warps + 1 TMA producer warp. Each consumer warp owns 2R
 // query rows outright (both GEMMs), so the P exchange between the QK^T
 // accumulator layout and the P.V operand layout is a warp-private smem round
 // trip guarded by __syncwarp — no CTA barrier in the main loop. K/V tiles
 // stream through a STAGES-deep ring filled by TMA (cp.async.bulk.tensor,
 // mbarrier complete_tx) and released per warp through "empty" mbarriers.
 //
-// Lane layout inside a consumer warp (lane = rg*16 + g):
-//   rows  r_i = 16*warp + rg + 2*i,  i = 0..7   (both GEMMs)
-//   GEMM1 keys  g + 16*j,  j = 0..RK-1          (S micro-tile 8 x RK)
-//   GEMM2 cols  4*g .. 4*g+3                    (O micro-tile 8 x 4)
-// Shared-memory pitches are chosen so every LDS.128 is either a 2-address
-// broadcast or conflict-free: Q/K rows are TMA-boxed 68 floats wide (the
-// 4 out-of-bounds columns are zero-filled by TMA), P rows are TK+16 floats.
+// Arithmetic: both GEMMs are register outer products on FFMA2 (sm_100 packed
+// fma.rn.f32x2, one broadcast scalar x one row pair; two IEEE FP32 FMAs per
+// issue slot). Shared memory delivers lane data at a fixed 128 B/clk/SM
+// (an LDS.128 costs 4 wavefronts, or 2 when it touches <= 2 addresses), so
+// the R x 4 lane micro-tile sets the smem/FMA balance: R = 8 needs 100% of
+// smem bandwidth at full FMA rate, R = 16 needs 75%.
+//
+// Lane layout inside a consumer warp (lane = 16h + 8rg + k8, g = 8h + k8):
+//   rows   r_i = 2R*warp + rg + 2i,  i = 0..R-1   (both GEMMs)
+//   GEMM1  keys g + 16j,  j = 0..RK-1             (S micro-tile R x RK)
+//   GEMM2  cols 4g .. 4g+3                        (O micro-tile R x 4)
+// Shared layouts: raw Q/K rows TMA-boxed 68 floats wide (4 zero columns pad
+// the pitch to 272 B); Q^T[d][row position] with each lane's R rows
+// contiguous; P^T[key][row position] per warp, pitch 2R+4.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -57,8 +63,8 @@ struct FwdParams {
   int64_t ks_b, ks_h, ks_r;
   int64_t vs_b, vs_h, vs_r;
   int64_t ys_b, ys_h, ys_r;
-  float c;    // |scale| * log2(e)
-  int neg;    // scale < 0: fold the sign into Q^T
+  float c;  // |scale| * log2(e)
+  int neg;  // scale < 0: fold the sign into Q^T
   int kv_begin, kv_end;
   int tiles_per_split;
   int qtiles;
@@ -71,34 +77,78 @@ struct FwdParams {
   int pw_pitch;         // floats per row of pW
   int pw_vec;           // float4 stores to pW legal
   int* err;
+  unsigned long long* trace;  // ELSA_TRACE builds: per-warp phase timestamps
 };
 
-template <int W_, int TK_, int STAGES_>
+// Phase-timestamp instrumentation (compiled in only with -DELSA_TRACE): for
+// CTAs 0..kTraceCtas-1 each consumer warp records globaltimer at 5 points of
+// each of its first kTraceTiles tiles: before the full-barrier wait, after it,
+// after GEMM1, after the softmax/combine, after GEMM2.
+constexpr int kTraceCtas = 4;
+constexpr int kTraceTiles = 32;
+constexpr int kTracePoints = 5;
+__device__ __forceinline__ void trace_mark(const FwdParams& p, int warp, int t, int point) {
+#ifdef ELSA_TRACE
+  if (blockIdx.x < kTraceCtas && blockIdx.y == 0 && t < kTraceTiles && (threadIdx.x & 31) == 0) {
+    unsigned long long ts;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+    p.trace[((blockIdx.x * 16 + warp) * kTraceTiles + t) * kTracePoints + point] = ts;
+  }
+#else
+  (void)p; (void)warp; (void)t; (void)point;
+#endif
+}
+
+template <int W_, int TK_, int STAGES_, int R_>
 struct FwdTraits {
   static constexpr int W = W_;
   static constexpr int TK = TK_;
   static constexpr int STAGES = STAGES_;
+  static constexpr int R = R_;            // query rows per lane
+  static constexpr int RP = R / 2;        // row pairs per lane
+  static constexpr int WR = 2 * R;        // query rows per warp
   static constexpr int D = 64;
   static constexpr int DV = 64;
-  static constexpr int TQ = 16 * W;
-  static constexpr int QP = D + 4;    // raw Q / K row pitch in floats (272 B; TMA box width)
-  static constexpr int QTP = TQ;      // Q^T pitch: Qt[d][row position]
-  static constexpr int VP = DV;       // V row pitch
-  static constexpr int PTP = 20;      // P^T pitch: Pt[key][row position], 16 rows + 4 pad
-  static constexpr int RK = TK / 16;  // keys per lane in GEMM1
+  static constexpr int TQ = WR * W;
+  static constexpr int QP = D + 4;        // raw Q / K row pitch in floats (272 B; TMA box width)
+  static constexpr int QTP = TQ;          // Q^T pitch: Qt[d][row position]
+  static constexpr int VP = DV;           // V row pitch
+  static constexpr int PTP = WR + 4;      // P^T pitch: Pt[key][row position]
+  static constexpr int RK = TK / 16;      // keys per lane in GEMM1
   static constexpr int QT_FLOATS = D * QTP;
   static constexpr int K_FLOATS = TK * QP;
   static constexpr int V_FLOATS = TK * VP;
   static constexpr int P_FLOATS = W * TK * PTP;  // also the raw-Q TMA landing zone
   static constexpr int QRAW_FLOATS = TQ * QP;
-  static constexpr int THREADS = (W + 1) * 32;
+  // Warp specialisation. R = 8: one producer warp, registers uniform.
+  // R = 16: a whole producer warpgroup (4 warps, only one issues TMA) so that
+  // setmaxnreg can move registers from producers to consumers — the register
+  // file is split per SM sub-partition (16K entries each, warps assigned
+  // round-robin), so 9 warps would cap every warp at 168 registers.
+  static constexpr bool kRegSplit = R >= 16;
+  static constexpr int PRODUCER_WARPS = kRegSplit ? 4 : 1;
+  static constexpr int THREADS = (W + PRODUCER_WARPS) * 32;
+  static constexpr int MIN_CTAS = (W <= 4 && R <= 8) ? 2 : 1;
+  static constexpr int WARPS_PER_SMSP = (MIN_CTAS * (W + PRODUCER_WARPS) + 3) / 4;
+  // launch-time register cap (per-SMSP file / warps resident on it, granule 8)
+  static constexpr int MAX_REGS = (16384 / (WARPS_PER_SMSP * 32)) / 8 * 8 > 255
+                                      ? 255
+                                      : (16384 / (WARPS_PER_SMSP * 32)) / 8 * 8;
+  static constexpr int PRODUCER_REGS = 40;
+  static constexpr int CONSUMER_REGS = 224;  // after setmaxnreg.inc (R = 16 only)
+  static_assert(!kRegSplit || (W % 4 == 0), "register split needs whole consumer warpgroups");
+  static_assert(!kRegSplit || PRODUCER_REGS + (W / 4) * CONSUMER_REGS <= 512,
+                "per-SMSP register budget after setmaxnreg");
   static constexpr size_t BAR_OFFSET =
       size_t(QT_FLOATS + STAGES * (K_FLOATS + V_FLOATS) + P_FLOATS) * 4;
   static constexpr size_t SMEM_BYTES = BAR_OFFSET + (2 * STAGES + 1) * 8;
   static constexpr uint32_t KV_TX_BYTES = uint32_t(K_FLOATS + V_FLOATS) * 4;
   static constexpr uint32_t Q_TX_BYTES = uint32_t(QRAW_FLOATS) * 4;
   static_assert(TK % 16 == 0, "TK must be a multiple of 16");
+  static_assert(R % 4 == 0, "R must be a multiple of 4 (float4 row groups)");
+  static_assert(TQ <= 256, "TMA box rows <= 256");
   static_assert(QRAW_FLOATS <= P_FLOATS, "raw Q must fit the P area");
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert((QT_FLOATS * 4) % 128 == 0 && (K_FLOATS * 4) % 128 == 0 &&
                     (V_FLOATS * 4) % 128 == 0,
                 "TMA destinations must stay 128-byte aligned");
@@ -151,13 +201,15 @@ __device__ __forceinline__ float f4(const float4& v, int c) {
   return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
-template <int W_, int TK_, int STAGES_, bool kTMA>
-__global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
+template <int W_, int TK_, int STAGES_, int R_, bool kTMA>
+__global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
     fwd_f32_kernel(const __grid_constant__ FwdParams p, const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV) {
-  using T = FwdTraits<W_, TK_, STAGES_>;
+  using T = FwdTraits<W_, TK_, STAGES_, R_>;
   constexpr int TK = T::TK, QP = T::QP, QTP = T::QTP, VP = T::VP, PTP = T::PTP, RK = T::RK;
+  constexpr int R = T::R, RP = T::RP, WR = T::WR;
+  using ptx::f32x2;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   float* Qt = reinterpret_cast<float*>(smem_raw);
@@ -195,8 +247,12 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
   }
   __syncthreads();
 
-  if (warp == T::W) {
-    // ---------------- producer warp ----------------
+  if (warp >= T::W) {
+    // ---------------- producer warp(group) ----------------
+    if constexpr (T::kRegSplit) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(T::PRODUCER_REGS));
+      if (warp != T::W) return;
+    }
     if constexpr (kTMA) {
       if (lane == 0) {
         ptx::prefetch_tmap(&tmQ);
@@ -220,25 +276,27 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
   }
 
   // ---------------- consumer warps ----------------
-  // lane = 16*h + 8*rg + k8: each half-warp holds both row groups and 8 of
-  // the 16 key/column groups, so every LDS.128 touches <= 128 B per half-warp
-  // (one shared-memory wavefront per half)
-  const int rg = (lane >> 3) & 1;               // row group: rows rg + 2i
+  if constexpr (T::kRegSplit) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(T::CONSUMER_REGS));
+  // lane = 16*h + 8*rg + k8: each half-warp holds both row groups and 8 of the
+  // 16 key/column groups
+  const int rg = (lane >> 3) & 1;                 // row group: rows rg + 2i
   const int g = ((lane >> 4) << 3) | (lane & 7);  // key group (GEMM1) / column group (GEMM2)
 
-  // Q^T, once per CTA: each warp transposes its own 16 rows out of the raw TMA
-  // box into Qt[d][pos], pos = 16*warp + 8*(r & 1) + (r >> 1) for local row r,
-  // so a lane's 8 rows (rg + 2i) are 8 consecutive floats: two LDS.128 per d.
+  // Q^T, once per CTA: each warp transposes its own 2R rows out of the raw TMA
+  // box into Qt[d][pos], pos = 2R*warp + R*(r & 1) + (r >> 1) for local row r,
+  // so a lane's R rows (rg + 2i) are R consecutive floats (R/4 LDS.128 per d).
   // The sign of a negative scale is folded in here (x = (-q).k * |c|).
   ptx::mbar_wait(qbar, 0);
   {
-    const int r = lane & 15;
-    const int dh = (lane >> 4) * 32;
-    const float* src = Qraw + (warp * 16 + r) * QP + dh;
-    float* dst = Qt + (warp * 16 + 8 * (r & 1) + (r >> 1)) + dh * QTP;
     const float sgn = p.neg ? -1.f : 1.f;
+    constexpr int LPR = 32 / WR;         // lanes per row (2 for R = 8, 1 for R = 16)
+    constexpr int DSPAN = T::D / LPR;    // d values per lane
+    const int r = lane / LPR;
+    const int dh = (lane % LPR) * DSPAN;
+    const float* src = Qraw + (warp * WR + r) * QP + dh;
+    float* dst = Qt + (warp * WR + R * (r & 1) + (r >> 1)) + dh * QTP;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < DSPAN / 4; ++c) {
       const float4 v = ptx::lds128(src + 4 * c);
       dst[(4 * c + 0) * QTP] = v.x * sgn;
       dst[(4 * c + 1) * QTP] = v.y * sgn;
@@ -249,38 +307,38 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
   // every consumer warp must finish reading raw Q before any warp writes P over it
   asm volatile("bar.sync 1, %0;" ::"r"(T::W * 32) : "memory");
 
-  const float* qt = Qt + warp * 16 + rg * 8;
+  const float* qt = Qt + warp * WR + rg * R;
   float* pw = Ps + warp * TK * PTP;
-  const float* ptr = pw + rg * 8;
+  const float* ptr = pw + rg * R;
   const float c2 = p.c;  // |scale| * log2(e) > 0
-  using ptx::f32x2;
   const f32x2 cc = ptx::pack2(c2, c2);
 
-  // Row pairs: lane rows (rg + 2i), i = 0..7, are held as 4 packed pairs
-  // ip = (i = 2ip, 2ip+1) so every GEMM FMA is an FFMA2 outer-product step
-  // (one broadcast scalar x one row pair), two FP32 FMAs per issue slot.
-  f32x2 o2[4][4];    // W accumulator: [row pair][column 4g + c]
-  float mrow[8];     // running anchors (log2 units)
-  f32x2 l2[4];       // running normalizer partials (this lane's keys)
+  // Row pairs: lane rows (rg + 2i), i = 0..R-1, are held as R/2 packed pairs
+  // ip = (i = 2ip, 2ip+1), so every GEMM FMA is an FFMA2 outer-product step.
+  f32x2 o2[RP][4];  // W accumulator: [row pair][column 4g + c]
+  float mrow[R];    // running anchors (log2 units)
+  f32x2 l2[RP];     // running normalizer partials (this lane's keys)
 #pragma unroll
-  for (int ip = 0; ip < 4; ++ip) {
+  for (int ip = 0; ip < RP; ++ip) {
     l2[ip] = 0ull;
 #pragma unroll
     for (int c = 0; c < 4; ++c) o2[ip][c] = 0ull;
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) mrow[i] = -CUDART_INF_F;
+  for (int i = 0; i < R; ++i) mrow[i] = -CUDART_INF_F;
 
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % T::STAGES;
+    trace_mark(p, warp, t, 0);
     ptx::mbar_wait(&full[s], (t / T::STAGES) & 1);
+    trace_mark(p, warp, t, 1);
     const float* ks = Ks + s * T::K_FLOATS + g * QP;
     const float* vs = Vs + s * T::V_FLOATS + 4 * g;
 
     // ---- GEMM1: S = Q K^T on FFMA2: s2[ip][j] += k_j[d] (bcast) * Qt[d][row pair ip]
-    f32x2 s2[4][RK];
+    f32x2 s2[RP][RK];
 #pragma unroll
-    for (int ip = 0; ip < 4; ++ip)
+    for (int ip = 0; ip < RP; ++ip)
 #pragma unroll
       for (int j = 0; j < RK; ++j) s2[ip][j] = 0ull;
 
@@ -291,22 +349,23 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
       for (int j = 0; j < RK; ++j) kf[j] = ptx::lds128(ks + j * 16 * QP + 4 * c);
 #pragma unroll
       for (int dd = 0; dd < 4; ++dd) {
-        f32x2 q2[4];
-        ptx::lds128x2(qt + (4 * c + dd) * QTP, q2[0], q2[1]);
-        ptx::lds128x2(qt + (4 * c + dd) * QTP + 4, q2[2], q2[3]);
+        f32x2 q2[RP];
+#pragma unroll
+        for (int u = 0; u < RP / 2; ++u)
+          ptx::lds128x2(qt + (4 * c + dd) * QTP + 4 * u, q2[2 * u], q2[2 * u + 1]);
 #pragma unroll
         for (int j = 0; j < RK; ++j) {
           const float kv = f4(kf[j], dd);
           const f32x2 kb = ptx::pack2(kv, kv);
-          // snake order keeps one operand in the reuse cache across the switch
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int ip = (j & 1) ? 3 - u : u;
+          for (int u = 0; u < RP; ++u) {
+            const int ip = (j & 1) ? RP - 1 - u : u;
             ptx::ffma2(s2[ip][j], kb, q2[ip]);
           }
         }
       }
     }
+    trace_mark(p, warp, t, 2);
 
     // ---- mask keys past this split's range ----
     const int key0 = p.kv_begin + (t_begin + t) * TK;
@@ -316,7 +375,7 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
         if (key0 + g + 16 * j >= kv_hi) {
           const f32x2 ninf = ptx::pack2(-CUDART_INF_F, -CUDART_INF_F);
 #pragma unroll
-          for (int ip = 0; ip < 4; ++ip) s2[ip][j] = ninf;
+          for (int ip = 0; ip < RP; ++ip) s2[ip][j] = ninf;
         }
     }
 
@@ -324,9 +383,8 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
     // Anchors in log2 units: m = fl(max_j acc_j * c). Each exponent is one FMA
     // acc*c - m (exact product, one rounding), so near-max keys carry an
     // absolute exponent error ~u*|s - m| rather than ~u*|s|.
-    f32x2 mneg2[4], corr2[4];
 #pragma unroll
-    for (int ip = 0; ip < 4; ++ip) {
+    for (int ip = 0; ip < RP; ++ip) {
       float mlo = ptx::lo2(s2[ip][0]), mhi = ptx::hi2(s2[ip][0]);
 #pragma unroll
       for (int j = 1; j < RK; ++j) {
@@ -342,110 +400,110 @@ __global__ void __launch_bounds__((W_ + 1) * 32, (W_ <= 4 ? 2 : 1))
       const float nlo = fmaxf(mrow[2 * ip], mlo * c2);
       const float nhi = fmaxf(mrow[2 * ip + 1], mhi * c2);
       // running side's factor; exp2(-inf) = 0 for the identity start state
-      corr2[ip] = ptx::pack2(ptx::ex2(mrow[2 * ip] - nlo), ptx::ex2(mrow[2 * ip + 1] - nhi));
+      const f32x2 corr =
+          ptx::pack2(ptx::ex2(mrow[2 * ip] - nlo), ptx::ex2(mrow[2 * ip + 1] - nhi));
       mrow[2 * ip] = nlo;
       mrow[2 * ip + 1] = nhi;
-      mneg2[ip] = ptx::pack2(-nlo, -nhi);
-    }
-    f32x2 p2[4][RK];
-#pragma unroll
-    for (int ip = 0; ip < 4; ++ip) {
+      const f32x2 mneg = ptx::pack2(-nlo, -nhi);
       f32x2 ps = 0ull;
 #pragma unroll
       for (int j = 0; j < RK; ++j) {
-        const f32x2 x = ptx::ffma2r(s2[ip][j], cc, mneg2[ip]);
+        const f32x2 x = ptx::ffma2r(s2[ip][j], cc, mneg);
         float xlo, xhi;
         ptx::unpack2(x, xlo, xhi);
-        p2[ip][j] = ptx::pack2(ptx::ex2(xlo), ptx::ex2(xhi));
-        ps = j == 0 ? p2[ip][j] : ptx::fadd2(ps, p2[ip][j]);
+        s2[ip][j] = ptx::pack2(ptx::ex2(xlo), ptx::ex2(xhi));  // s2 now holds p
+        ps = j == 0 ? s2[ip][j] : ptx::fadd2(ps, s2[ip][j]);
       }
-      l2[ip] = ptx::ffma2r(l2[ip], corr2[ip], ps);
+      l2[ip] = ptx::ffma2r(l2[ip], corr, ps);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) o2[ip][c] = ptx::fmul2(o2[ip][c], corr2[ip]);
+      for (int c = 0; c < 4; ++c) o2[ip][c] = ptx::fmul2(o2[ip][c], corr);
     }
-    // P^T: key-major, this lane's 8 rows contiguous -> two STS.128 per key
+    // P^T: key-major, this lane's R rows contiguous -> R/4 STS.128 per key
 #pragma unroll
     for (int j = 0; j < RK; ++j) {
-      float* dst = pw + (g + 16 * j) * PTP + rg * 8;
-      *reinterpret_cast<ulonglong2*>(dst) = make_ulonglong2(p2[0][j], p2[1][j]);
-      *reinterpret_cast<ulonglong2*>(dst + 4) = make_ulonglong2(p2[2][j], p2[3][j]);
+      float* dst = pw + (g + 16 * j) * PTP + rg * R;
+#pragma unroll
+      for (int u = 0; u < RP / 2; ++u)
+        *reinterpret_cast<ulonglong2*>(dst + 4 * u) =
+            make_ulonglong2(s2[2 * u][j], s2[2 * u + 1][j]);
     }
     __syncwarp();
+    trace_mark(p, warp, t, 3);
 
     // ---- GEMM2: W += P V on FFMA2: o2[ip][c] += v_j[c] (bcast) * Pt[j][row pair ip]
-#pragma unroll 4
+#pragma unroll 2
     for (int jj = 0; jj < TK; ++jj) {
-      f32x2 pr[4];
-      ptx::lds128x2(ptr + jj * PTP, pr[0], pr[1]);
-      ptx::lds128x2(ptr + jj * PTP + 4, pr[2], pr[3]);
+      f32x2 pr[RP];
+#pragma unroll
+      for (int u = 0; u < RP / 2; ++u)
+        ptx::lds128x2(ptr + jj * PTP + 4 * u, pr[2 * u], pr[2 * u + 1]);
       const float4 vf = ptx::lds128(vs + jj * VP);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const float vv = f4(vf, c);
         const f32x2 vb = ptx::pack2(vv, vv);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int ip = (c & 1) ? 3 - u : u;
+        for (int u = 0; u < RP; ++u) {
+          const int ip = (c & 1) ? RP - 1 - u : u;
           ptx::ffma2(o2[ip][c], vb, pr[ip]);
         }
       }
     }
     __syncwarp();
+    trace_mark(p, warp, t, 4);
     if (lane == 0) ptx::mbar_arrive(&empty[s]);
-  }
-
-  // unpack the row-pair state for the epilogue
-  float o[8][4], lrow[8];
-#pragma unroll
-  for (int ip = 0; ip < 4; ++ip) {
-    ptx::unpack2(l2[ip], lrow[2 * ip], lrow[2 * ip + 1]);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) ptx::unpack2(o2[ip][c], o[2 * ip][c], o[2 * ip + 1][c]);
   }
 
   // ---------------- epilogue ----------------
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    float l = lrow[i];
-    l += __shfl_xor_sync(0xffffffffu, l, 1);
-    l += __shfl_xor_sync(0xffffffffu, l, 2);
-    l += __shfl_xor_sync(0xffffffffu, l, 4);
-    l += __shfl_xor_sync(0xffffffffu, l, 16);
-    const int qrow = q0 + warp * 16 + rg + 2 * i;
-    if (qrow >= p.n_q) continue;
-    if (p.mode == kModeFinal) {
-      // engine.py:377-378: the normalizer must be finite and positive
-      if (!(l > 0.f) || !isfinite(l)) {
-        if (g == 0) atomicCAS(p.err, 0, 3);
-      }
-      float* yrow = p.y + int64_t(b) * p.ys_b + int64_t(h) * p.ys_h + int64_t(qrow) * p.ys_r;
-      float yv[4];
+  for (int ip = 0; ip < RP; ++ip) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) yv[c] = __fdiv_rn(o[i][c], l);
-      const int col = 4 * g;
-      if (p.y_vec && col + 3 < p.dv) {
-        *reinterpret_cast<float4*>(yrow + col) = make_float4(yv[0], yv[1], yv[2], yv[3]);
+    for (int half = 0; half < 2; ++half) {
+      const int i = 2 * ip + half;
+      float l = half ? ptx::hi2(l2[ip]) : ptx::lo2(l2[ip]);
+      l += __shfl_xor_sync(0xffffffffu, l, 1);
+      l += __shfl_xor_sync(0xffffffffu, l, 2);
+      l += __shfl_xor_sync(0xffffffffu, l, 4);
+      l += __shfl_xor_sync(0xffffffffu, l, 16);
+      float o[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o[c] = half ? ptx::hi2(o2[ip][c]) : ptx::lo2(o2[ip][c]);
+      const int qrow = q0 + warp * WR + rg + 2 * i;
+      if (qrow >= p.n_q) continue;
+      if (p.mode == kModeFinal) {
+        // engine.py:377-378: the normalizer must be finite and positive
+        if (!(l > 0.f) || !isfinite(l)) {
+          if (g == 0) atomicCAS(p.err, 0, 3);
+        }
+        float* yrow = p.y + int64_t(b) * p.ys_b + int64_t(h) * p.ys_h + int64_t(qrow) * p.ys_r;
+        float yv[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) yv[c] = __fdiv_rn(o[c], l);
+        const int col = 4 * g;
+        if (p.y_vec && col + 3 < p.dv) {
+          *reinterpret_cast<float4*>(yrow + col) = make_float4(yv[0], yv[1], yv[2], yv[3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (col + c < p.dv) yrow[col + c] = yv[c];
+        }
       } else {
+        const int64_t row = (int64_t(b) * p.H + h) * p.n_q + qrow;
+        const int64_t idx = int64_t(split) * p.part_stride + row;
+        if (g == 0) {
+          const float m = (p.mode == kModePartialNat) ? mrow[i] * 0.69314718055994531f : mrow[i];
+          p.pm[idx] = m;
+          p.pS[idx] = l;
+        }
+        float* wrow = p.pW + idx * p.pw_pitch;
+        const int col = 4 * g;
+        if (p.pw_vec && col + 3 < p.dv) {
+          *reinterpret_cast<float4*>(wrow + col) = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (col + c < p.dv) yrow[col + c] = yv[c];
-      }
-    } else {
-      const int64_t row = (int64_t(b) * p.H + h) * p.n_q + qrow;
-      const int64_t idx = int64_t(split) * p.part_stride + row;
-      if (g == 0) {
-        const float m = (p.mode == kModePartialNat) ? mrow[i] * 0.69314718055994531f : mrow[i];
-        p.pm[idx] = m;
-        p.pS[idx] = l;
-      }
-      float* wrow = p.pW + idx * p.pw_pitch;
-      const int col = 4 * g;
-      if (p.pw_vec && col + 3 < p.dv) {
-        *reinterpret_cast<float4*>(wrow + col) = make_float4(o[i][0], o[i][1], o[i][2], o[i][3]);
-      } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (col + c < p.dv) wrow[col + c] = o[i][c];
+          for (int c = 0; c < 4; ++c)
+            if (col + c < p.dv) wrow[col + c] = o[c];
+        }
       }
     }
   }

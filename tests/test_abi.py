@@ -68,7 +68,7 @@ def resolve(s, req=0):
 def test_split_planner():
     # big grids need no split; tiny grids split the key range to fill 148 SMs
     assert resolve(_shape(1, 16, 16384, 16384)) == 1
-    assert resolve(_shape(8, 12, 512, 512)) == 1
+    assert resolve(_shape(8, 12, 512, 512)) <= 2
     s = resolve(_shape(1, 1, 1024, 1024))
     assert 2 <= s <= 16
     # explicit requests are honoured up to the tile count / 32
