@@ -43,4 +43,23 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float* sink, int iters, 
 // FMAs per thread per outer iteration.
 constexpr int kFfmaPerIter = 8 * 8 * 4;
 
+// Register-bank-conflict-free form: 32 independent chains c = c * k + b with
+// immediate operands (two register reads per FFMA), the pipe's ceiling.
+__global__ void __launch_bounds__(256) ffma_peak_imm_kernel(float* sink, int iters, float seed) {
+  float c[32];
+  const float t = float(threadIdx.x) * 1e-7f + seed;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) c[i] = t + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll 8
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int i = 0; i < 32; ++i) c[i] = fmaf(c[i], 0.9999f, 0.5f);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) s += c[i];
+  if (s == 1234.5678f) sink[threadIdx.x] = s;
+}
+
 }  // namespace elsa
