@@ -339,7 +339,7 @@ def main():
                        "one kernel launch per step at this shape",
     }
 
-    # ---- sweep (kernel-only, L2 flushed between iterations) ----
+    # ---- sweep (kernel-only: CUDA-graph replays, L2 flushed between them) ----
     sweep = []
     if not args.no_sweep and world == 1:
         flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
@@ -350,23 +350,33 @@ def main():
             vv = torch.randn(bb, hh, nn, 64, device=dev)
             for _ in range(3):
                 elsa.scaled_dot_product_attention(qq, kk, vv)
-            reps = 20 if nn <= 4096 else 6
-            times = []
+            torch.cuda.synchronize()
+            # capture one call so host-side Python overhead stays out of the
+            # measurement; replays are enqueued back to back (no host idle gaps)
+            graph = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(dev)
+            with torch.cuda.stream(cap):
+                with torch.cuda.graph(graph, stream=cap):
+                    elsa.scaled_dot_product_attention(qq, kk, vv)
+            torch.cuda.synchronize()
+            reps = 30 if nn <= 4096 else 8
+            evs = []
             for _ in range(reps):
                 flush.fill_(1.0)
                 s0 = torch.cuda.Event(enable_timing=True)
                 s1 = torch.cuda.Event(enable_timing=True)
                 s0.record(stream)
-                elsa.scaled_dot_product_attention(qq, kk, vv)
+                graph.replay()
                 s1.record(stream)
-                torch.cuda.synchronize()
-                times.append(s0.elapsed_time(s1))
+                evs.append((s0, s1))
+            torch.cuda.synchronize()
+            times = [a.elapsed_time(b) for a, b in evs[2:]]
             t_ms = float(np.median(times))
             tf = flops(bb, hh, nn, nn) / (t_ms * 1e-3) / 1e12
             sweep.append({"B": bb, "H": hh, "n": nn, "ms": t_ms, "tflops": tf,
                           "frac_ffma_peak": tf / spec_peak,
                           "plan": elsa.describe_plan(qq, kk, vv)})
-            del qq, kk, vv
+            del qq, kk, vv, graph
         # GPU comparator on the same box: torch SDPA FP32 (TF32 off), the paper's ME-SDPA
         try:
             torch.backends.cuda.matmul.allow_tf32 = False

@@ -41,8 +41,8 @@ thread_local char t_last_cuda_error[256] = "";
 unsigned long long* g_trace = nullptr;
 unsigned long long* trace_buffer() {
   if (!g_trace) {
-    cudaMalloc(&g_trace, sizeof(unsigned long long) * kTraceCtas * 16 * kTraceTiles * kTracePoints);
-    cudaMemset(g_trace, 0, sizeof(unsigned long long) * kTraceCtas * 16 * kTraceTiles * kTracePoints);
+    cudaMalloc(&g_trace, sizeof(unsigned long long) * kTraceWords);
+    cudaMemset(g_trace, 0, sizeof(unsigned long long) * kTraceWords);
   }
   return g_trace;
 }
@@ -120,16 +120,17 @@ int forced_cfg() {
 
 struct CfgInfo {
   int tq, tk, ctas_per_sm;
-  double eff;  // measured relative per-SM throughput at n = 16K
+  double tile_us;  // SM-time for one TQ x 64 tile (measured on B200 at 1965 MHz)
+  double cta_us;   // per-CTA prologue/epilogue SM-time
 };
 CfgInfo cfg_info(int cfg) {
   switch (cfg) {
     case kCfgW8R16:
-      return {256, 64, 1, 1.02};
+      return {256, 64, 1, 12.2, 10.0};
     case kCfgW8R8:
-      return {128, 64, 1, 0.99};
+      return {128, 64, 1, 6.45, 4.0};
     default:
-      return {64, 64, 2, 1.0};
+      return {64, 64, 2, 3.23, 2.0};
   }
 }
 
@@ -148,15 +149,13 @@ bool valid_shape(const elsa_shape* s) {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Launch plan (config + kv split count). Cost model in units of one
-// 64-row x 64-key tile on a whole SM:
-//   waves(cfg, s) * (ceil(tiles / s) + kCtaOverheadTiles) * (TQ / 64) * ctas_per_sm / eff
-// + [s > 1] * (1 + s * rows * kSplitUnitsPerRow)     partial-state round trip + merge pass
+// Launch plan (config + kv split count). Cost model in microseconds, fitted
+// to B200 measurements (tools/plan_sweep.py):
+//   ceil(CTAs * s / 148) * (ceil(tiles / s) * tile_us + cta_us)     forward kernel
+// + [s > 1] * (4 + s * rows * 528 B / 3 TB/s)                        partial states + merge
 // minimised over the configs and s <= min(tiles, 32), with
 // s >= ceil(tiles / kMaxChainTiles) so no CTA folds more than kMaxChainTiles
 // tiles sequentially (bounded chain depth; the rest is the log-depth tree).
-constexpr double kCtaOverheadTiles = 2.0;
-constexpr double kSplitUnitsPerRow = 3.4e-5;  // 528 B/row at ~5 TB/s over a ~3.1 us unit
 constexpr int64_t kMaxChainTiles = 256;
 
 struct Plan {
@@ -166,11 +165,9 @@ struct Plan {
 
 double plan_cost(const CfgInfo& ci, int64_t ctas, int64_t tiles, int64_t rows, int64_t sms,
                  int64_t s) {
-  const int64_t slots = sms * ci.ctas_per_sm;
-  double t = double(ceil_div(ctas * s, slots)) *
-             (double(ceil_div(tiles, s)) + kCtaOverheadTiles) * (ci.tq / 64.0) *
-             ci.ctas_per_sm / ci.eff;
-  if (s > 1) t += 1.0 + double(s) * double(rows) * kSplitUnitsPerRow;
+  double t = double(ceil_div(ctas * s, sms)) *
+             (double(ceil_div(tiles, s)) * ci.tile_us + ci.cta_us);
+  if (s > 1) t += 4.0 + double(s) * double(rows) * 528.0 / 3.0e6;
   return t;
 }
 
@@ -189,7 +186,6 @@ Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms) {
   const int forced = forced_cfg();
   for (int cfg = 0; cfg < kCfgCount; ++cfg) {
     if (forced != kCfgAuto && cfg != forced) continue;
-    if (forced == kCfgAuto && cfg == kCfgW8R8) continue;  // never better than the other two
     const CfgInfo ci = cfg_info(cfg);
     const int64_t ctas = ceil_div(sh->n_q, ci.tq) * sh->B * sh->H;
     const int64_t tiles = ceil_div(kv_len, ci.tk);
@@ -302,7 +298,12 @@ int launch_merge(MergeParams& mp, cudaStream_t stream) {
   constexpr int kWarps = 8;
   const int64_t blocks = ceil_div(mp.rows, kWarps);
   if (blocks >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
-  merge_f32_kernel<<<unsigned(blocks), kWarps * 32, 0, stream>>>(mp);
+  auto kern = mp.parts <= 2    ? merge_f32_kernel<2>
+              : mp.parts <= 4  ? merge_f32_kernel<4>
+              : mp.parts <= 8  ? merge_f32_kernel<8>
+              : mp.parts <= 16 ? merge_f32_kernel<16>
+                               : merge_f32_kernel<32>;
+  kern<<<unsigned(blocks), kWarps * 32, 0, stream>>>(mp);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "merge launch");
   ++t_last_launches;
   return ELSA_OK;
@@ -648,7 +649,7 @@ int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n
 int elsa_dev_read_trace(unsigned long long* out, size_t n) {
 #ifdef ELSA_TRACE
   if (!g_trace) return ELSA_ERR_SHAPE;
-  const size_t total = size_t(kTraceCtas) * 16 * kTraceTiles * kTracePoints;
+  const size_t total = kTraceWords;
   if (n > total) n = total;
   return cudaMemcpy(out, g_trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
                  cudaSuccess

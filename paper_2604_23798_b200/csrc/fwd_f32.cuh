@@ -87,6 +87,24 @@ struct FwdParams {
 constexpr int kTraceCtas = 4;
 constexpr int kTraceTiles = 32;
 constexpr int kTracePoints = 5;
+constexpr int kTraceMaxCtas = 8192;  // CTA start/end stamps follow the per-warp block
+constexpr size_t kTraceWords = size_t(kTraceCtas) * 16 * kTraceTiles * kTracePoints + 3 * kTraceMaxCtas;
+__device__ __forceinline__ void trace_cta(const FwdParams& p, int what) {
+#ifdef ELSA_TRACE
+  const unsigned cta = blockIdx.x + gridDim.x * blockIdx.y;
+  if (cta < kTraceMaxCtas && threadIdx.x == 0) {
+    unsigned long long ts;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned long long* base = p.trace + size_t(kTraceCtas) * 16 * kTraceTiles * kTracePoints;
+    base[3 * cta + what] = ts;
+    if (what == 0) base[3 * cta + 2] = smid;
+  }
+#else
+  (void)p; (void)what;
+#endif
+}
 __device__ __forceinline__ void trace_mark(const FwdParams& p, int warp, int t, int point) {
 #ifdef ELSA_TRACE
   if (blockIdx.x < kTraceCtas && blockIdx.y == 0 && t < kTraceTiles && (threadIdx.x & 31) == 0) {
@@ -135,6 +153,10 @@ struct FwdTraits {
                                       ? 255
                                       : (16384 / (WARPS_PER_SMSP * 32)) / 8 * 8;
   static constexpr int PRODUCER_REGS = 40;
+  // Phase-offsetting the two warps of each SMSP (see `lagged` in the kernel)
+  // measured no gain on B200 (per-warp phase trace) and costs registers, so
+  // it is compiled out.
+  static constexpr bool kLag = false;
   static constexpr int CONSUMER_REGS = 224;  // after setmaxnreg.inc (R = 16 only)
   static_assert(!kRegSplit || (W % 4 == 0), "register split needs whole consumer warpgroups");
   static_assert(!kRegSplit || PRODUCER_REGS + (W / 4) * CONSUMER_REGS <= 512,
@@ -237,6 +259,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
   const int ntiles = max(t_end - t_begin, 0);
   const int kv_hi = min(p.kv_end, p.kv_begin + t_end * TK);
 
+  trace_cta(p, 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < T::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
@@ -327,13 +350,47 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
 #pragma unroll
   for (int i = 0; i < R; ++i) mrow[i] = -CUDART_INF_F;
 
+  // ---- GEMM2 of tile tt: W += P V on FFMA2, o2[ip][c] += v_j[c] (bcast) *
+  // Pt[j][row pair ip]; then release the tile's K/V stage to the producer.
+  auto gemm2_release = [&](int tt) {
+    const int st = tt % T::STAGES;
+    const float* vs = Vs + st * T::V_FLOATS + 4 * g;
+#pragma unroll 2
+    for (int jj = 0; jj < TK; ++jj) {
+      f32x2 pr[RP];
+#pragma unroll
+      for (int u = 0; u < RP / 2; ++u)
+        ptx::lds128x2(ptr + jj * PTP + 4 * u, pr[2 * u], pr[2 * u + 1]);
+      const float4 vf = ptx::lds128(vs + jj * VP);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float vv = f4(vf, c);
+        const f32x2 vb = ptx::pack2(vv, vv);
+#pragma unroll
+        for (int u = 0; u < RP; ++u) {
+          const int ip = (c & 1) ? RP - 1 - u : u;
+          ptx::ffma2(o2[ip][c], vb, pr[ip]);
+        }
+      }
+    }
+    __syncwarp();
+    trace_mark(p, warp, tt, 4);
+    if (lane == 0) ptx::mbar_arrive(&empty[st]);
+  };
+
+  // Phase offset between the two warps that share an SM sub-partition (warps
+  // w and w + 4, W >= 8): the upper half runs GEMM2 of the previous tile
+  // before GEMM1 of the current one, so its latency-bound softmax section
+  // overlaps the partner's FFMA2 stream instead of coinciding with it.
+  const bool lagged = T::kLag && warp >= T::W / 2;
+
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % T::STAGES;
+    if (lagged && t > 0) gemm2_release(t - 1);
     trace_mark(p, warp, t, 0);
     ptx::mbar_wait(&full[s], (t / T::STAGES) & 1);
     trace_mark(p, warp, t, 1);
     const float* ks = Ks + s * T::K_FLOATS + g * QP;
-    const float* vs = Vs + s * T::V_FLOATS + 4 * g;
 
     // ---- GEMM1: S = Q K^T on FFMA2: s2[ip][j] += k_j[d] (bcast) * Qt[d][row pair ip]
     f32x2 s2[RP][RK];
@@ -429,30 +486,9 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
     }
     __syncwarp();
     trace_mark(p, warp, t, 3);
-
-    // ---- GEMM2: W += P V on FFMA2: o2[ip][c] += v_j[c] (bcast) * Pt[j][row pair ip]
-#pragma unroll 2
-    for (int jj = 0; jj < TK; ++jj) {
-      f32x2 pr[RP];
-#pragma unroll
-      for (int u = 0; u < RP / 2; ++u)
-        ptx::lds128x2(ptr + jj * PTP + 4 * u, pr[2 * u], pr[2 * u + 1]);
-      const float4 vf = ptx::lds128(vs + jj * VP);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float vv = f4(vf, c);
-        const f32x2 vb = ptx::pack2(vv, vv);
-#pragma unroll
-        for (int u = 0; u < RP; ++u) {
-          const int ip = (c & 1) ? RP - 1 - u : u;
-          ptx::ffma2(o2[ip][c], vb, pr[ip]);
-        }
-      }
-    }
-    __syncwarp();
-    trace_mark(p, warp, t, 4);
-    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    if (!lagged) gemm2_release(t);
   }
+  if (lagged && ntiles > 0) gemm2_release(ntiles - 1);
 
   // ---------------- epilogue ----------------
 #pragma unroll
@@ -507,6 +543,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
       }
     }
   }
+  trace_cta(p, 1);
 }
 
 }  // namespace elsa

@@ -54,16 +54,17 @@ __device__ __forceinline__ float merge_factor(float mx, float m, bool log2_domai
   return log2_domain ? exp2f(mx - m) : expf(mx - m);
 }
 
+template <int MAXP>
 __global__ void __launch_bounds__(256) merge_f32_kernel(const MergeParams p) {
   const int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= p.rows) return;
   const bool lg = p.log2_domain != 0;
 
-  float am[kMergeMaxParts], aS[kMergeMaxParts], a0[kMergeMaxParts], a1[kMergeMaxParts];
+  float am[MAXP], aS[MAXP], a0[MAXP], a1[MAXP];
   const int c0 = lane, c1 = lane + 32;
 #pragma unroll
-  for (int i = 0; i < kMergeMaxParts; ++i) {
+  for (int i = 0; i < MAXP; ++i) {
     if (i < p.parts) {
       const int64_t idx = int64_t(i) * p.part_stride + row;
       am[i] = p.m[idx];
@@ -81,11 +82,12 @@ __global__ void __launch_bounds__(256) merge_f32_kernel(const MergeParams p) {
 
   // Balanced pairwise tree, in place: slot i <- slot 2i (+) slot 2i+1.
   int k = p.parts;
+  constexpr int LEVELS = MAXP <= 1 ? 0 : (MAXP <= 2 ? 1 : (MAXP <= 4 ? 2 : (MAXP <= 8 ? 3 : (MAXP <= 16 ? 4 : 5))));
 #pragma unroll
-  for (int level = 0; level < 5; ++level) {
+  for (int level = 0; level < LEVELS; ++level) {
     if (k <= 1) break;
 #pragma unroll
-    for (int i = 0; i < kMergeMaxParts / 2; ++i) {
+    for (int i = 0; i < MAXP / 2; ++i) {
       if (2 * i + 1 < k) {
         const float ma = am[2 * i], mb = am[2 * i + 1];
         const float mm = fmaxf(ma, mb);

@@ -115,3 +115,17 @@ if __name__ == "__main__":
         if a:
             print(f"  region {r[0][0]:#x}-{r[-1][0]:#x}: {a} packed, {b} cycles "
                   f"({200.0 * a / b:.1f}%), {len(r)} instructions")
+
+
+def loops(insts):
+    """(start, end) address ranges of backward-branch loop bodies."""
+    out = []
+    for a, t in insts:
+        if "BRA" in t:
+            import re as _re
+            m = _re.search(r"0x([0-9a-f]+)", t.split("BRA")[1])
+            if m:
+                tgt = int(m.group(1), 16)
+                if tgt < a:
+                    out.append((tgt, a))
+    return out

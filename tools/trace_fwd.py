@@ -41,3 +41,5 @@ print(f"tile total mean {tot.mean():8.0f} ns")
 st = a[0, :, :, 1]
 print("CTA0 start skew per tile (ns):", (st.max(axis=0) - st.min(axis=0))[:12].tolist())
 print("CTA0 softmax start (rel ns), tile 5:", ((a[0, :, 5, 2] - a[0, :, 5, 1].min())).tolist())
+# absolute timeline of CTA 0: kernel-relative first/last marks
+print("CTA0 warp0 first mark -> last mark (ns):", int(a[0, 0][a[0, 0] > 0].max() - a[0, 0][a[0, 0] > 0].min()))
