@@ -157,10 +157,22 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // s >= ceil(tiles / kMaxChainTiles) so no CTA folds more than kMaxChainTiles
 // tiles sequentially (bounded chain depth; the rest is the log-depth tree).
 constexpr int64_t kMaxChainTiles = 256;
+// Split workspace budget for auto planning (partial states are
+// (2 + 64) * 4 B per row per split): 4 GiB unless ELSA_MAX_WORKSPACE_MB says
+// otherwise. Explicit kv_splits requests are not capped.
+int64_t workspace_budget() {
+  static const int64_t b = [] {
+    const char* e = std::getenv("ELSA_MAX_WORKSPACE_MB");
+    const long long mb = e ? std::atoll(e) : 4096;
+    return int64_t(mb > 0 ? mb : 0) * 1024 * 1024;
+  }();
+  return b;
+}
 
 struct Plan {
   int cfg;
   int splits;
+  int64_t heads_per_batch;  // (b, h) pairs per launch batch when splits > 1
 };
 
 double plan_cost(const CfgInfo& ci, int64_t ctas, int64_t tiles, int64_t rows, int64_t sms,
@@ -181,30 +193,42 @@ int64_t normalize_splits(int64_t s, int64_t tiles) {
 }
 
 Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms) {
-  Plan best{kCfgW4R8, 1};
+  const int64_t BH = sh->B * sh->H;
+  Plan best{kCfgW4R8, 1, BH > 0 ? BH : 1};
   double best_t = 1e300;
   const int forced = forced_cfg();
+  const int64_t head_bytes = sh->n_q * (2 + 64) * 4;  // one split of one (b, h) head
   for (int cfg = 0; cfg < kCfgCount; ++cfg) {
     if (forced != kCfgAuto && cfg != forced) continue;
     const CfgInfo ci = cfg_info(cfg);
-    const int64_t ctas = ceil_div(sh->n_q, ci.tq) * sh->B * sh->H;
+    const int64_t ctas = ceil_div(sh->n_q, ci.tq) * BH;
     const int64_t tiles = ceil_div(kv_len, ci.tk);
-    const int64_t rows = sh->B * sh->H * sh->n_q;
-    if (ctas == 0 || tiles < 1) return Plan{forced == kCfgAuto ? int(kCfgW4R8) : forced, 1};
+    const int64_t rows = BH * sh->n_q;
+    if (ctas == 0 || tiles < 1) return Plan{forced == kCfgAuto ? int(kCfgW4R8) : forced, 1, 1};
     int64_t lo, hi;
     if (requested > 0) {
       lo = hi = normalize_splits(requested, tiles);
     } else {
       hi = tiles < kMaxSplits ? tiles : kMaxSplits;
+      // splits of even a single head must fit the workspace budget
+      const int64_t ws_cap = head_bytes > 0 ? workspace_budget() / head_bytes : hi;
+      if (hi > ws_cap) hi = ws_cap < 1 ? 1 : ws_cap;
       lo = ceil_div(tiles, kMaxChainTiles);
       if (lo > hi) lo = hi;
     }
     for (int64_t s = lo; s <= hi; ++s) {
       const int64_t sn = normalize_splits(s, tiles);
-      const double t = plan_cost(ci, ctas, tiles, rows, sms, sn);
+      int64_t hpb = BH;
+      if (sn > 1 && requested <= 0) {
+        hpb = workspace_budget() / (sn * head_bytes);
+        if (hpb < 1) hpb = 1;
+        if (hpb > BH) hpb = BH;
+      }
+      const int64_t batches = ceil_div(BH, hpb);
+      const double t = plan_cost(ci, ctas, tiles, rows, sms, sn) + 8.0 * double(batches - 1);
       if (t < best_t - 1e-9) {
         best_t = t;
-        best = Plan{cfg, int(sn)};
+        best = Plan{cfg, int(sn), hpb};
       }
     }
   }
@@ -245,7 +269,7 @@ bool encode_map(CUtensorMap* map, const float* base, int64_t inner, int64_t rows
 
 template <int W, int TK, int ST, int R>
 int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[3],
-                   int64_t v_st[3], int splits, int cfg_slot, DeviceCache* dc,
+                   int64_t v_st[3], int splits, int64_t bh_count, int cfg_slot, DeviceCache* dc,
                    cudaStream_t stream) {
   using T = FwdTraits<W, TK, ST, R>;
   p.qtiles = int(ceil_div(s->n_q, T::TQ));
@@ -271,7 +295,7 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fwd)");
     dc->attr[slot] = true;
   }
-  const int64_t gx = int64_t(p.qtiles) * s->B * s->H;
+  const int64_t gx = int64_t(p.qtiles) * bh_count;
   if (gx >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
   const dim3 grid{unsigned(gx), unsigned(splits), 1u};
   kern<<<grid, T::THREADS, T::SMEM_BYTES, stream>>>(p, maps[0], maps[1], maps[2]);
@@ -281,15 +305,19 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
 }
 
 int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[3],
-               int64_t v_st[3], const Plan& plan, DeviceCache* dc, cudaStream_t stream) {
+               int64_t v_st[3], const Plan& plan, int64_t bh_count, DeviceCache* dc,
+               cudaStream_t stream) {
   const int splits = plan.splits;
   switch (plan.cfg) {
     case kCfgW8R16:
-      return launch_fwd_cfg<8, 64, 2, 16>(p, s, q_st, k_st, v_st, splits, kCfgW8R16, dc, stream);
+      return launch_fwd_cfg<8, 64, 2, 16>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R16, dc,
+                                          stream);
     case kCfgW8R8:
-      return launch_fwd_cfg<8, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, kCfgW8R8, dc, stream);
+      return launch_fwd_cfg<8, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8, dc,
+                                         stream);
     default:
-      return launch_fwd_cfg<4, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, kCfgW4R8, dc, stream);
+      return launch_fwd_cfg<4, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW4R8, dc,
+                                         stream);
   }
 }
 
@@ -341,10 +369,111 @@ void fill_common(FwdParams& p, const float* q, const float* k, const float* v,
   p.trace = trace_buffer();
 }
 
-size_t split_ws_bytes(const elsa_shape* s, int splits) {
-  if (splits <= 1) return 0;
-  const size_t rows = size_t(s->B) * size_t(s->H) * size_t(s->n_q);
-  return size_t(splits) * rows * (2 + 64) * sizeof(float);
+size_t split_ws_bytes(const elsa_shape* s, const Plan& pl) {
+  if (pl.splits <= 1) return 0;
+  const size_t rows = size_t(pl.heads_per_batch) * size_t(s->n_q);
+  return size_t(pl.splits) * rows * (2 + 64) * sizeof(float);
+}
+
+// Shared driver of elsa_fwd_f32 (y != nullptr: final Y) and elsa_partial_f32
+// (m/S/W: natural-log partial states of keys [kv_begin, kv_end)). With
+// kv splits > 1 the work runs in batches of `heads_per_batch` (b, h) heads:
+// forward kernel -> split partial states in the workspace -> K2 tree merge.
+int run_forward(const float* q, const float* k, const float* v, const elsa_shape* shp,
+                double scale, int64_t kv_begin, int64_t kv_end, int kv_splits, void* workspace,
+                size_t ws_bytes, cudaStream_t strm, float* y, float* m_out, float* S_out,
+                float* W_out) {
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  int64_t q_st[3], k_st[3], v_st[3];
+  std::memcpy(q_st, shp->q_stride, sizeof(q_st));
+  std::memcpy(k_st, shp->k_stride, sizeof(k_st));
+  std::memcpy(v_st, shp->v_stride, sizeof(v_st));
+  sanitize(q_st, shp->n_q, shp->H, shp->B, shp->d);
+  sanitize(k_st, shp->n_kv, shp->H, shp->B, shp->d);
+  sanitize(v_st, shp->n_kv, shp->H, shp->B, shp->dv);
+
+  const int64_t BH = shp->B * shp->H;
+  const int64_t len = kv_end - kv_begin;
+  const Plan plan = len == 0 ? Plan{kCfgW4R8, 1, BH} : plan_for(shp, len, kv_splits, dc->sms);
+  const bool final_out = y != nullptr;
+  FwdParams p;
+  fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
+  p.kv_begin = int(kv_begin);
+  p.kv_end = int(kv_end);
+  p.err = dc->err;
+  if (final_out) {
+    p.y = y;
+    p.ys_b = shp->y_stride[0];
+    p.ys_h = shp->y_stride[1];
+    p.ys_r = shp->y_stride[2];
+    p.y_vec = (reinterpret_cast<uintptr_t>(y) % 16 == 0) && (p.ys_b % 4 == 0) &&
+              (p.ys_h % 4 == 0) && (p.ys_r % 4 == 0);
+  }
+  if (plan.splits <= 1) {
+    p.bh_begin = 0;
+    if (final_out) {
+      p.mode = kModeFinal;
+    } else {
+      p.mode = kModePartialNat;
+      p.pm = m_out;
+      p.pS = S_out;
+      p.pW = W_out;
+      p.part_stride = BH * shp->n_q;
+      p.pw_pitch = int(shp->dv);
+      p.pw_vec = (reinterpret_cast<uintptr_t>(W_out) % 16 == 0) && (shp->dv % 4 == 0);
+    }
+    return launch_fwd(p, shp, q_st, k_st, v_st, plan, BH, dc, strm);
+  }
+  const size_t need = split_ws_bytes(shp, plan);
+  if (!workspace || ws_bytes < need) return ELSA_ERR_WORKSPACE;
+  float* ws = static_cast<float*>(workspace);
+  const int splits = plan.splits;
+  for (int64_t bh0 = 0; bh0 < BH; bh0 += plan.heads_per_batch) {
+    const int64_t cnt = BH - bh0 < plan.heads_per_batch ? BH - bh0 : plan.heads_per_batch;
+    const int64_t rows = cnt * shp->n_q;
+    p.bh_begin = int(bh0);
+    p.mode = kModePartialLog2;
+    p.pm = ws;
+    p.pS = ws + int64_t(splits) * rows;
+    p.pW = ws + int64_t(splits) * rows * 2;
+    p.part_stride = rows;
+    p.pw_pitch = 64;
+    p.pw_vec = 1;
+    if (int st = launch_fwd(p, shp, q_st, k_st, v_st, plan, cnt, dc, strm)) return st;
+    MergeParams mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.m = p.pm;
+    mp.S = p.pS;
+    mp.W = p.pW;
+    mp.parts = splits;
+    mp.rows = rows;
+    mp.dv = int(shp->dv);
+    mp.w_pitch = 64;
+    mp.part_stride = rows;
+    mp.log2_domain = 1;
+    mp.err = dc->err;
+    if (final_out) {
+      mp.finalize = 1;
+      mp.y = y;
+      mp.H = int(shp->H);
+      mp.n_q = int(shp->n_q);
+      mp.bh_begin = int(bh0);
+      mp.ys_b = shp->y_stride[0];
+      mp.ys_h = shp->y_stride[1];
+      mp.ys_r = shp->y_stride[2];
+    } else {
+      const int64_t off = bh0 * shp->n_q;
+      mp.finalize = 0;
+      mp.m_out = m_out + off;
+      mp.S_out = S_out + off;
+      mp.W_out = W_out + off * shp->dv;
+      mp.out_pitch = int(shp->dv);
+      mp.out_log2_to_nat = 1;
+    }
+    if (int st = launch_merge(mp, strm)) return st;
+  }
+  return ELSA_OK;
 }
 
 }  // namespace
@@ -393,9 +522,11 @@ int elsa_resolve_kv_splits(const elsa_shape* shp, int requested) {
 }
 
 size_t elsa_workspace_bytes(const elsa_shape* shp, int kv_splits) {
-  const int s = elsa_resolve_kv_splits(shp, kv_splits);
-  if (s <= 1) return 0;
-  return split_ws_bytes(shp, s);
+  if (!valid_shape(shp) || kv_splits < 0) return 0;
+  DeviceCache* dc = nullptr;
+  int sms = 148;
+  if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
+  return split_ws_bytes(shp, plan_for(shp, shp->n_kv, kv_splits, sms));
 }
 
 int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
@@ -406,69 +537,8 @@ int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
   if (!q || !k || !v || !y) return ELSA_ERR_SHAPE;
   if (shp->y_stride[0] < 0 || shp->y_stride[2] < 0) return ELSA_ERR_SHAPE;
   if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
-  DeviceCache* dc = nullptr;
-  if (int st = current_device_cache(&dc)) return st;
-  cudaStream_t strm = static_cast<cudaStream_t>(stream);
-
-  int64_t q_st[3], k_st[3], v_st[3];
-  std::memcpy(q_st, shp->q_stride, sizeof(q_st));
-  std::memcpy(k_st, shp->k_stride, sizeof(k_st));
-  std::memcpy(v_st, shp->v_stride, sizeof(v_st));
-  sanitize(q_st, shp->n_q, shp->H, shp->B, shp->d);
-  sanitize(k_st, shp->n_kv, shp->H, shp->B, shp->d);
-  sanitize(v_st, shp->n_kv, shp->H, shp->B, shp->dv);
-
-  const Plan plan = plan_for(shp, shp->n_kv, kv_splits, dc->sms);
-  const int splits = plan.splits;
-  FwdParams p;
-  fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
-  p.kv_begin = 0;
-  p.kv_end = int(shp->n_kv);
-  p.err = dc->err;
-  p.y = y;
-  p.ys_b = shp->y_stride[0];
-  p.ys_h = shp->y_stride[1];
-  p.ys_r = shp->y_stride[2];
-  p.y_vec = (reinterpret_cast<uintptr_t>(y) % 16 == 0) && (p.ys_b % 4 == 0) &&
-            (p.ys_h % 4 == 0) && (p.ys_r % 4 == 0);
-
-  if (splits <= 1) {
-    p.mode = kModeFinal;
-    return launch_fwd(p, shp, q_st, k_st, v_st, plan, dc, strm);
-  }
-  const size_t need = split_ws_bytes(shp, splits);
-  if (!workspace || ws_bytes < need) return ELSA_ERR_WORKSPACE;
-  const int64_t rows = shp->B * shp->H * shp->n_q;
-  float* ws = static_cast<float*>(workspace);
-  p.mode = kModePartialLog2;
-  p.pm = ws;
-  p.pS = ws + int64_t(splits) * rows;
-  p.pW = ws + int64_t(splits) * rows * 2;
-  p.part_stride = rows;
-  p.pw_pitch = 64;
-  p.pw_vec = 1;
-  if (int st = launch_fwd(p, shp, q_st, k_st, v_st, plan, dc, strm)) return st;
-
-  MergeParams mp;
-  std::memset(&mp, 0, sizeof(mp));
-  mp.m = p.pm;
-  mp.S = p.pS;
-  mp.W = p.pW;
-  mp.parts = splits;
-  mp.rows = rows;
-  mp.dv = int(shp->dv);
-  mp.w_pitch = 64;
-  mp.part_stride = rows;
-  mp.log2_domain = 1;
-  mp.finalize = 1;
-  mp.y = y;
-  mp.H = int(shp->H);
-  mp.n_q = int(shp->n_q);
-  mp.ys_b = shp->y_stride[0];
-  mp.ys_h = shp->y_stride[1];
-  mp.ys_r = shp->y_stride[2];
-  mp.err = dc->err;
-  return launch_merge(mp, strm);
+  return run_forward(q, k, v, shp, scale, 0, shp->n_kv, kv_splits, workspace, ws_bytes,
+                     static_cast<cudaStream_t>(stream), y, nullptr, nullptr, nullptr);
 }
 
 int elsa_partial_f32(const float* q, const float* k, const float* v, const elsa_shape* shp,
@@ -478,68 +548,9 @@ int elsa_partial_f32(const float* q, const float* k, const float* v, const elsa_
   if (!valid_shape(shp) || kv_splits < 0 || !std::isfinite(scale)) return ELSA_ERR_SHAPE;
   if (kv_begin < 0 || kv_end < kv_begin || kv_end > shp->n_kv) return ELSA_ERR_SHAPE;
   if (!q || !k || !v || !m || !S || !W) return ELSA_ERR_SHAPE;
-  const int64_t rows = shp->B * shp->H * shp->n_q;
-  if (rows == 0) return ELSA_OK;
-  DeviceCache* dc = nullptr;
-  if (int st = current_device_cache(&dc)) return st;
-  cudaStream_t strm = static_cast<cudaStream_t>(stream);
-
-  int64_t q_st[3], k_st[3], v_st[3];
-  std::memcpy(q_st, shp->q_stride, sizeof(q_st));
-  std::memcpy(k_st, shp->k_stride, sizeof(k_st));
-  std::memcpy(v_st, shp->v_stride, sizeof(v_st));
-  sanitize(q_st, shp->n_q, shp->H, shp->B, shp->d);
-  sanitize(k_st, shp->n_kv, shp->H, shp->B, shp->d);
-  sanitize(v_st, shp->n_kv, shp->H, shp->B, shp->dv);
-
-  const int64_t len = kv_end - kv_begin;
-  const Plan plan = len == 0 ? Plan{kCfgW4R8, 1} : plan_for(shp, len, kv_splits, dc->sms);
-  const int splits = plan.splits;
-  FwdParams p;
-  fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
-  p.kv_begin = int(kv_begin);
-  p.kv_end = int(kv_end);
-  p.err = dc->err;
-  if (splits <= 1) {
-    p.mode = kModePartialNat;
-    p.pm = m;
-    p.pS = S;
-    p.pW = W;
-    p.part_stride = rows;
-    p.pw_pitch = int(shp->dv);
-    p.pw_vec = (reinterpret_cast<uintptr_t>(W) % 16 == 0) && (shp->dv % 4 == 0);
-    return launch_fwd(p, shp, q_st, k_st, v_st, plan, dc, strm);
-  }
-  const size_t need = split_ws_bytes(shp, splits);
-  if (!workspace || ws_bytes < need) return ELSA_ERR_WORKSPACE;
-  float* ws = static_cast<float*>(workspace);
-  p.mode = kModePartialLog2;
-  p.pm = ws;
-  p.pS = ws + int64_t(splits) * rows;
-  p.pW = ws + int64_t(splits) * rows * 2;
-  p.part_stride = rows;
-  p.pw_pitch = 64;
-  p.pw_vec = 1;
-  if (int st = launch_fwd(p, shp, q_st, k_st, v_st, plan, dc, strm)) return st;
-  MergeParams mp;
-  std::memset(&mp, 0, sizeof(mp));
-  mp.m = p.pm;
-  mp.S = p.pS;
-  mp.W = p.pW;
-  mp.parts = splits;
-  mp.rows = rows;
-  mp.dv = int(shp->dv);
-  mp.w_pitch = 64;
-  mp.part_stride = rows;
-  mp.log2_domain = 1;
-  mp.finalize = 0;
-  mp.m_out = m;
-  mp.S_out = S;
-  mp.W_out = W;
-  mp.out_pitch = int(shp->dv);
-  mp.out_log2_to_nat = 1;
-  mp.err = dc->err;
-  return launch_merge(mp, strm);
+  if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
+  return run_forward(q, k, v, shp, scale, kv_begin, kv_end, kv_splits, workspace, ws_bytes,
+                     static_cast<cudaStream_t>(stream), nullptr, m, S, W);
 }
 
 int elsa_merge_f32(const float* m, const float* S, const float* W, int parts, int64_t rows,
@@ -640,7 +651,8 @@ int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n
   const Plan pl = plan_for(shp, shp->n_kv, kv_splits, sms);
   static const char* names[] = {"w4r8", "w8r16", "w8r8"};
   const CfgInfo ci = cfg_info(pl.cfg);
-  std::snprintf(buf, n, "%s tq=%d tk=%d kv_splits=%d", names[pl.cfg], ci.tq, ci.tk, pl.splits);
+  std::snprintf(buf, n, "%s tq=%d tk=%d kv_splits=%d heads_per_batch=%lld", names[pl.cfg], ci.tq,
+                ci.tk, pl.splits, static_cast<long long>(pl.heads_per_batch));
   return ELSA_OK;
 }
 

@@ -66,6 +66,7 @@ struct FwdParams {
   float c;  // |scale| * log2(e)
   int neg;  // scale < 0: fold the sign into Q^T
   int kv_begin, kv_end;
+  int bh_begin;  // first flattened (b, h) index of this launch (row batching)
   int tiles_per_split;
   int qtiles;
   int mode;
@@ -247,7 +248,8 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
   const int lane = threadIdx.x & 31;
 
   const int qtile = blockIdx.x % p.qtiles;
-  const int bh = blockIdx.x / p.qtiles;
+  const int bh_rel = blockIdx.x / p.qtiles;
+  const int bh = bh_rel + p.bh_begin;
   const int split = blockIdx.y;
   const int b = bh / p.H;
   const int h = bh - b * p.H;
@@ -524,7 +526,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
             if (col + c < p.dv) yrow[col + c] = yv[c];
         }
       } else {
-        const int64_t row = (int64_t(b) * p.H + h) * p.n_q + qrow;
+        const int64_t row = int64_t(bh_rel) * p.n_q + qrow;  // relative to this batch
         const int64_t idx = int64_t(split) * p.part_stride + row;
         if (g == 0) {
           const float m = (p.mode == kModePartialNat) ? mrow[i] * 0.69314718055994531f : mrow[i];

@@ -328,3 +328,39 @@ def test_kv_sharded_single_process_matches():
     q, k, v = gpu(Q), gpu(K), gpu(V)
     y = edist.kv_sharded_attention(q, k, v, 0, 1000, chunks=8)
     assert_bound(y.cpu().numpy(), oracle.naive_attention(Q, K, V), 1000, "kv-sharded")
+
+
+# ---------------------------------------------------------------- long context (C4 on one GPU)
+def _sampled_check(q, k, v, n, heads, rows_per_head, y, what):
+    rng = np.random.default_rng(n)
+    rows = [(0, h, int(r)) for h in heads for r in
+            sorted(set([0, n - 1] + rng.integers(0, n, rows_per_head).tolist()))]
+    Kh = {h: k[0, h].double().cpu().numpy() for h in heads}
+    Vh = {h: v[0, h].double().cpu().numpy() for h in heads}
+    sc = 1.0 / math.sqrt(q.shape[-1])
+    errs = []
+    for b, h, r in rows:
+        qv = q[0, h, r].double().cpu().numpy()
+        s = (Kh[h] @ qv) * sc
+        s -= s.max()
+        p = np.exp(s)
+        ref = (p @ Vh[h]) / p.sum()
+        got = y[0, h, r].double().cpu().numpy()
+        errs.append(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+    thr = oracle.bound_threshold(n)
+    assert max(errs) <= thr, f"{what}: max sampled row err {max(errs):.3e} > {thr:.3e}"
+    return max(errs)
+
+
+def test_c4_64k_single_gpu_and_kv_chunked_path():
+    from paper_2604_23798_b200 import dist as edist
+    n, H = 65536, 16
+    g = torch.Generator(device=DEV)
+    g.manual_seed(64)
+    q, k, v = (torch.randn(1, H, n, 64, device=DEV, generator=g) for _ in range(3))
+    y = elsa.scaled_dot_product_attention(q, k, v, check_numerics=True)
+    _sampled_check(q, k, v, n, [0, H - 1], 6, y, "C4 direct")
+    # the KV-sharded pipeline on one rank (8 key chunks, K2 merge tree)
+    y2 = edist.kv_sharded_attention(q, k, v, 0, n, chunks=8)
+    _sampled_check(q, k, v, n, [3], 6, y2, "C4 kv-chunked")
+    assert torch.allclose(y, y2, rtol=1e-4, atol=1e-5)
