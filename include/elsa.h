@@ -102,6 +102,14 @@ int elsa_partial_f32(const float* q, const float* k, const float* v,
                      int kv_splits, void* workspace, size_t ws_bytes,
                      void* stream);
 
+/* FP16 / BF16 variant: the QK^T and PV contractions on the
+ * tcgen05 tensor cores with FP32 accumulation in TMEM; the (m, S, W) states,
+ * their combine and the epilogue in FP32. q, k, v, y are 16-bit
+ * (is_bf16 ? bfloat16 : float16) with d = dv = 64, 16-byte aligned bases and
+ * strides; y is written in the same format. */
+int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y,
+                 const elsa_shape* shp, double scale, int is_bf16, void* stream);
+
 /* Merge `parts` partial states per row with the reference's balanced
  * pairwise tree (adjacent pairs, odd tail passes through; monoid.py:234-265)
  * and its identity-guarded combine (monoid.py:160-200). Inputs are laid out

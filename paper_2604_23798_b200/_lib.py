@@ -28,6 +28,7 @@ EXPORTED_SYMBOLS = (
     "elsa_workspace_bytes",
     "elsa_fwd_f32",
     "elsa_partial_f32",
+    "elsa_fwd_f16",
     "elsa_merge_f32",
     "elsa_get_device_error",
     "elsa_ffma_peak",
@@ -86,6 +87,8 @@ def _declare(h):
     h.elsa_partial_f32.restype = c_int
     h.elsa_partial_f32.argtypes = [c_vp, c_vp, c_vp, shp, c_dbl, c_i64, c_i64,
                                    c_vp, c_vp, c_vp, c_int, c_vp, c_sz, c_vp]
+    h.elsa_fwd_f16.restype = c_int
+    h.elsa_fwd_f16.argtypes = [c_vp, c_vp, c_vp, c_vp, shp, c_dbl, c_int, c_vp]
     h.elsa_merge_f32.restype = c_int
     h.elsa_merge_f32.argtypes = [c_vp, c_vp, c_vp, c_int, c_i64, c_int, c_i64, c_int,
                                  c_vp, c_vp, c_vp, c_vp, c_vp]

@@ -54,14 +54,22 @@ def _as_4d(t, name):
     raise ShapeError(f"{name} must have at least 2 dimensions, got shape {tuple(t.shape)}")
 
 
-def _validate(q, k, v):
+_TC_DTYPES = (torch.float16, torch.bfloat16)
+
+
+def _validate(q, k, v, allow_16bit=False):
     for name, t in (("query", q), ("key", k), ("value", v)):
         if not isinstance(t, torch.Tensor):
             raise ShapeError(f"{name} must be a torch.Tensor")
-        if t.dtype != torch.float32:
+        ok = t.dtype == torch.float32 or (allow_16bit and t.dtype in _TC_DTYPES)
+        if not ok:
             raise ShapeError(
-                f"{name} dtype {t.dtype}: the ELSA FP32 path takes torch.float32 only "
-                "(no TF32/FP16 fallback)")
+                f"{name} dtype {t.dtype}: the ELSA path takes torch.float32 (FP32 FFMA kernel)"
+                + (" or float16 / bfloat16 (tcgen05 kernel)" if allow_16bit else "")
+                + " only (no fallback)")
+    if not (q.dtype == k.dtype == v.dtype):
+        raise ShapeError("query, key and value must share one dtype")
+    for name, t in (("query", q), ("key", k), ("value", v)):
         if not t.is_cuda:
             raise ShapeError(f"{name} is on {t.device}: libelsa runs on CUDA devices only "
                              "(no CPU fallback)")
@@ -156,7 +164,7 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
     if is_causal:
         raise ShapeError("is_causal is not supported: the reference computes full "
                          "(bidirectional) attention only")
-    _validate(query, key, value)
+    _validate(query, key, value, allow_16bit=True)
     orig_dim = query.dim()
     orig_shape = query.shape
     q, k, v = (_prep(_as_4d(t, n)) for t, n in ((query, "query"), (key, "key"), (value, "value")))
@@ -168,6 +176,13 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
         raise ShapeError(f"scale must be finite, got {sc}")
     B, H, n_q, _ = q.shape
     dv = v.shape[-1]
+    if q.dtype in _TC_DTYPES:
+        y = _sdpa_tc(q, k, v, sc, out)
+        if check_numerics:
+            check_device_error(q.device)
+        if orig_dim == 4 or out is not None:
+            return y
+        return y.reshape(*orig_shape[:-1], dv)
     if out is None:
         y = torch.empty((B, H, n_q, dv), device=q.device, dtype=torch.float32)
     else:
@@ -193,6 +208,31 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
     if orig_dim == 4 or out is not None:
         return y
     return y.reshape(*orig_shape[:-1], dv)
+
+
+def _sdpa_tc(q, k, v, sc, out):
+    """FP16 / BF16 inputs: K5 on the tcgen05 tensor cores (FP32 accumulation
+    and FP32 (m, S, W) state; output in the input format)."""
+    B, H, n_q, d = q.shape
+    dv = v.shape[-1]
+    if d != 64 or dv != 64:
+        raise ShapeError(f"the 16-bit tensor-core path needs d = dv = 64, got d={d}, dv={dv}")
+    q, k, v = (t if t.stride(-1) == 1 and t.data_ptr() % 16 == 0 and all(
+        (s * 2) % 16 == 0 for s in t.stride()[:3]) else t.contiguous() for t in (q, k, v))
+    if out is None:
+        y = torch.empty((B, H, n_q, dv), device=q.device, dtype=q.dtype)
+    else:
+        y = out
+        if tuple(y.shape) != (B, H, n_q, dv) or y.dtype != q.dtype or y.device != q.device:
+            raise ShapeError("out must match the query's dtype/device with shape (B, H, n_q, dv)")
+    shp = _shape(q, k, v, y)
+    with torch.cuda.device(q.device):
+        st = _lib.lib().elsa_fwd_f16(
+            ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),
+            ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(y.data_ptr()), ctypes.byref(shp),
+            ctypes.c_double(sc), 1 if q.dtype == torch.bfloat16 else 0, _stream_ptr(q.device))
+        _lib.check_status(st, "elsa_fwd_f16")
+    return y
 
 
 def partial_states(query, key, value, kv_begin=0, kv_end=None, scale=None, kv_splits=1):

@@ -20,6 +20,7 @@
 #include "elsa.h"
 #include "ffma_peak.cuh"
 #include "fwd_f32.cuh"
+#include "fwd_tc.cuh"
 #include "merge_f32.cuh"
 
 namespace elsa {
@@ -375,6 +376,28 @@ size_t split_ws_bytes(const elsa_shape* s, const Plan& pl) {
   return size_t(pl.splits) * rows * (2 + 64) * sizeof(float);
 }
 
+bool encode_map16(CUtensorMap* map, const void* base, int64_t rows, int64_t H, int64_t B,
+                  const int64_t st[3], bool bf16) {
+  auto enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {64, cuuint64_t(rows), cuuint64_t(H), cuuint64_t(B)};
+  cuuint64_t strides[3] = {cuuint64_t(st[2] * 2), cuuint64_t(st[1] * 2), cuuint64_t(st[0] * 2)};
+  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                   const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool aligned16(const void* ptr, const int64_t st[3]) {
+  if (reinterpret_cast<uintptr_t>(ptr) % 16) return false;
+  for (int i = 0; i < 3; ++i)
+    if (st[i] <= 0 || (st[i] * 2) % 16 || st[i] * 2 >= (int64_t(1) << 40)) return false;
+  return true;
+}
+
 // Shared driver of elsa_fwd_f32 (y != nullptr: final Y) and elsa_partial_f32
 // (m/S/W: natural-log partial states of keys [kv_begin, kv_end)). With
 // kv splits > 1 the work runs in batches of `heads_per_batch` (b, h) heads:
@@ -551,6 +574,65 @@ int elsa_partial_f32(const float* q, const float* k, const float* v, const elsa_
   if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
   return run_forward(q, k, v, shp, scale, kv_begin, kv_end, kv_splits, workspace, ws_bytes,
                      static_cast<cudaStream_t>(stream), nullptr, m, S, W);
+}
+
+int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const elsa_shape* shp,
+                 double scale, int is_bf16, void* stream) {
+  t_last_launches = 0;
+  if (!valid_shape(shp) || !std::isfinite(scale)) return ELSA_ERR_SHAPE;
+  if (shp->d != 64 || shp->dv != 64) return ELSA_ERR_SHAPE;
+  if (!q || !k || !v || !y) return ELSA_ERR_SHAPE;
+  if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  int64_t q_st[3], k_st[3], v_st[3], y_st[3];
+  std::memcpy(q_st, shp->q_stride, sizeof(q_st));
+  std::memcpy(k_st, shp->k_stride, sizeof(k_st));
+  std::memcpy(v_st, shp->v_stride, sizeof(v_st));
+  std::memcpy(y_st, shp->y_stride, sizeof(y_st));
+  sanitize(q_st, shp->n_q, shp->H, shp->B, 64);
+  sanitize(k_st, shp->n_kv, shp->H, shp->B, 64);
+  sanitize(v_st, shp->n_kv, shp->H, shp->B, 64);
+  sanitize(y_st, shp->n_q, shp->H, shp->B, 64);
+  if (!aligned16(q, q_st) || !aligned16(k, k_st) || !aligned16(v, v_st) || !aligned16(y, y_st))
+    return ELSA_ERR_SHAPE;
+  const bool bf16 = is_bf16 != 0;
+  CUtensorMap maps[3];
+  if (!encode_map16(&maps[0], q, shp->n_q, shp->H, shp->B, q_st, bf16) ||
+      !encode_map16(&maps[1], k, shp->n_kv, shp->H, shp->B, k_st, bf16) ||
+      !encode_map16(&maps[2], v, shp->n_kv, shp->H, shp->B, v_st, bf16))
+    return ELSA_ERR_SHAPE;
+  TcParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.y = y;
+  p.B = int(shp->B);
+  p.H = int(shp->H);
+  p.n_q = int(shp->n_q);
+  p.n_kv = int(shp->n_kv);
+  p.ys_b = y_st[0];
+  p.ys_h = y_st[1];
+  p.ys_r = y_st[2];
+  double c = std::fabs(scale) * kLog2e;
+  if (c < 1e-30) c = 1e-30;
+  p.c = float(c);
+  p.neg = scale < 0 ? 1 : 0;
+  p.qtiles = int(ceil_div(shp->n_q, TcTraits::TQ));
+  p.err = dc->err;
+  auto kern = bf16 ? fwd_tc_kernel<true> : fwd_tc_kernel<false>;
+  const int slot = 6 + (bf16 ? 1 : 0);
+  if (!dc->attr[slot]) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(TcTraits::SMEM_BYTES));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc)");
+    dc->attr[slot] = true;
+  }
+  const int64_t gx = int64_t(p.qtiles) * shp->B * shp->H;
+  if (gx >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
+  kern<<<unsigned(gx), TcTraits::THREADS, TcTraits::SMEM_BYTES,
+         static_cast<cudaStream_t>(stream)>>>(p, maps[0], maps[1], maps[2]);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "tc launch");
+  ++t_last_launches;
+  return ELSA_OK;
 }
 
 int elsa_merge_f32(const float* m, const float* S, const float* W, int parts, int64_t rows,

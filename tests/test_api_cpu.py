@@ -24,9 +24,13 @@ def test_non_goals_raise(kw):
         elsa.scaled_dot_product_attention(t(1, 1, 4, 8), t(1, 1, 4, 8), t(1, 1, 4, 8), **kw)
 
 
-def test_non_fp32_rejected():
+def test_unsupported_dtypes_rejected():
     with pytest.raises(elsa.ShapeError, match="float32"):
-        elsa.scaled_dot_product_attention(*(t(1, 1, 4, 8, dtype=torch.float16),) * 3)
+        elsa.scaled_dot_product_attention(*(t(1, 1, 4, 8, dtype=torch.float64),) * 3)
+    with pytest.raises(elsa.ShapeError, match="no CPU fallback"):
+        elsa.scaled_dot_product_attention(*(t(1, 1, 4, 64, dtype=torch.bfloat16),) * 3)
+    with pytest.raises(elsa.ShapeError, match="share one dtype"):
+        elsa.scaled_dot_product_attention(t(1, 1, 4, 64), t(1, 1, 4, 64), t(1, 1, 4, 64, dtype=torch.bfloat16))
 
 
 def test_errors_mirror_reference_taxonomy():

@@ -1,0 +1,61 @@
+"""K5: the FP16 / BF16 variant on the tcgen05 tensor cores,
+checked against the FP64 oracle on the same (16-bit-rounded) inputs. The
+16-bit P operand and 16-bit output bound the accuracy; the gate is 2x the
+error of PyTorch's own 16-bit SDPA on the same inputs (plus an absolute floor
+at the output format's unit roundoff)."""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2604_23798_b200 as elsa  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def _check(dtype, B, H, n_q, n_kv, seed, scale=None):
+    g = torch.Generator(device=DEV)
+    g.manual_seed(seed)
+    q = torch.randn(B, H, n_q, 64, device=DEV, generator=g).to(dtype)
+    k = torch.randn(B, H, n_kv, 64, device=DEV, generator=g).to(dtype)
+    v = torch.randn(B, H, n_kv, 64, device=DEV, generator=g).to(dtype)
+    y = elsa.scaled_dot_product_attention(q, k, v, scale=scale, check_numerics=True)
+    assert y.dtype == dtype and y.shape == (B, H, n_q, 64)
+    ref = oracle.naive_attention(*(t.double().cpu().numpy() for t in (q, k, v)), scale=scale)
+    ours = oracle.row_rel_err(y.double().cpu().numpy(), ref)
+    theirs = oracle.row_rel_err(torch.nn.functional.scaled_dot_product_attention(
+        q, k, v, scale=scale).double().cpu().numpy(), ref)
+    u = 2.0 ** -8 if dtype == torch.bfloat16 else 2.0 ** -11
+    assert np.percentile(ours, 99) <= max(2 * np.percentile(theirs, 99), u), (
+        np.percentile(ours, 99), np.percentile(theirs, 99))
+    assert ours.max() <= max(2 * theirs.max(), 2 * u)
+    return ours.max()
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("B,H,n_q,n_kv", [(1, 2, 128, 128), (1, 4, 1024, 1024), (2, 3, 200, 333),
+                                          (1, 1, 1, 1), (1, 2, 129, 4096)])
+def test_tc_matches_fp64(dtype, B, H, n_q, n_kv):
+    _check(dtype, B, H, n_q, n_kv, seed=n_q * 31 + n_kv)
+
+
+def test_tc_negative_scale_and_determinism():
+    _check(torch.bfloat16, 1, 2, 256, 256, seed=3, scale=-0.2)
+    q = torch.randn(1, 2, 300, 64, device=DEV, dtype=torch.bfloat16)
+    a = elsa.scaled_dot_product_attention(q, q, q)
+    b = elsa.scaled_dot_product_attention(q, q, q)
+    assert torch.equal(a, b)
+
+
+def test_tc_rejects_other_head_dims():
+    q = torch.randn(1, 1, 16, 32, device=DEV, dtype=torch.bfloat16)
+    with pytest.raises(elsa.ShapeError):
+        elsa.scaled_dot_product_attention(q, q, q)
