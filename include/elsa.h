@@ -121,6 +121,31 @@ int elsa_merge_f32(const float* m, const float* S, const float* W,
                    int finalize, float* y, float* m_out, float* S_out,
                    float* W_out, void* stream);
 
+/* Per-key-block partial states for every query row:
+ * block j covers keys [j*block_size, min((j+1)*block_size, n_kv)); natural-log
+ * anchors. Layout, nblocks = ceil(n_kv / block_size), rows = B*H*n_q in
+ * (b, h, q) order: m[row*nblocks + j], S[...], W[(row*nblocks + j)*dv + c].
+ * Replaces engine.blockwise_states (engine.py:430-451), which returns the same
+ * per-block totals for one query and one (b, h). */
+int elsa_blockwise_f32(const float* q, const float* k, const float* v,
+                       const elsa_shape* shp, double scale, int64_t block_size,
+                       float* m, float* S, float* W, void* stream);
+
+/* Workspace for elsa_block_scan_f32: rows * 2^ceil(log2 nblocks) * (2 + dv)
+ * floats. */
+size_t elsa_block_scan_workspace_bytes(int64_t rows, int nblocks, int dv);
+
+/* The reference's two-pass inter-block combine per row over nblocks states
+ * ([rows][nblocks] layout as elsa_blockwise_f32 writes, natural anchors):
+ * identity-padded up-sweep -> total (engine.py:179-199, 265-293) and, when
+ * pre_m/pre_S/pre_W are non-NULL, the down-sweep's exclusive prefixes, identity
+ * first (engine.py:202-231, 294-297). Same tree shape as the reference. */
+int elsa_block_scan_f32(const float* m, const float* S, const float* W,
+                        int64_t rows, int nblocks, int dv,
+                        float* total_m, float* total_S, float* total_W,
+                        float* pre_m, float* pre_S, float* pre_W,
+                        void* workspace, size_t ws_bytes, void* stream);
+
 /* Synchronises `stream`, returns the device error word (0 = none, else an
  * elsa_status) through *code, and clears it. */
 int elsa_get_device_error(void* stream, int* code);

@@ -43,3 +43,4 @@ from .attention import (  # noqa: F401
     vectorized_probs,
 )
 from .scan_port import scan_forward_port  # noqa: F401
+from .blocks import blockwise_states_fp64, inter_block_combine  # noqa: F401

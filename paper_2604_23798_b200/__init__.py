@@ -14,6 +14,8 @@ Entry points:
 """
 
 from .attention import (  # noqa: F401
+    blockwise_states,
+    inter_block_combine,
     check_device_error,
     describe_plan,
     ffma_peak_tflops,

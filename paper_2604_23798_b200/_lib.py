@@ -30,6 +30,9 @@ EXPORTED_SYMBOLS = (
     "elsa_partial_f32",
     "elsa_fwd_f16",
     "elsa_merge_f32",
+    "elsa_blockwise_f32",
+    "elsa_block_scan_workspace_bytes",
+    "elsa_block_scan_f32",
     "elsa_get_device_error",
     "elsa_ffma_peak",
     "elsa_last_launch_count",
@@ -92,6 +95,13 @@ def _declare(h):
     h.elsa_merge_f32.restype = c_int
     h.elsa_merge_f32.argtypes = [c_vp, c_vp, c_vp, c_int, c_i64, c_int, c_i64, c_int,
                                  c_vp, c_vp, c_vp, c_vp, c_vp]
+    h.elsa_blockwise_f32.restype = c_int
+    h.elsa_blockwise_f32.argtypes = [c_vp, c_vp, c_vp, shp, c_dbl, c_i64, c_vp, c_vp, c_vp, c_vp]
+    h.elsa_block_scan_workspace_bytes.restype = c_sz
+    h.elsa_block_scan_workspace_bytes.argtypes = [c_i64, c_int, c_int]
+    h.elsa_block_scan_f32.restype = c_int
+    h.elsa_block_scan_f32.argtypes = [c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_vp, c_vp,
+                                      c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]
     h.elsa_get_device_error.restype = c_int
     h.elsa_get_device_error.argtypes = [c_vp, ctypes.POINTER(c_int)]
     h.elsa_ffma_peak.restype = c_int

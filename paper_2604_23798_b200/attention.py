@@ -28,6 +28,8 @@ __all__ = [
     "scaled_dot_product_attention",
     "partial_states",
     "merge_states",
+    "blockwise_states",
+    "inter_block_combine",
     "check_device_error",
     "resolve_kv_splits",
     "describe_plan",
@@ -132,6 +134,14 @@ def resolve_kv_splits(q, k, v, kv_splits=0):
     if r < 0:
         _lib.check_status(-r, "elsa_resolve_kv_splits")
     return r
+
+
+def workspace_bytes(q, k, v, kv_splits=0):
+    """Split workspace elsa_fwd_f32 needs for these shapes (0 = none)."""
+    q4, k4, v4 = _as_4d(q, "query"), _as_4d(k, "key"), _as_4d(v, "value")
+    shp = _shape(q4, k4, v4)
+    with torch.cuda.device(q4.device):
+        return int(_lib.lib().elsa_workspace_bytes(ctypes.byref(shp), int(kv_splits)))
 
 
 def describe_plan(q, k, v, kv_splits=0):
@@ -305,6 +315,74 @@ def merge_states(m, S, W, finalize=True):
             ctypes.c_void_p(Wo.data_ptr()), _stream_ptr(m.device))
         _lib.check_status(st, "elsa_merge_f32")
         return mo, So, Wo
+
+
+def blockwise_states(query, key, value, block_size=128, scale=None):
+    """Per-key-block (m, S, W) states for every query row — the GPU form of
+    ``engine.blockwise_states`` (engine.py:430-451), which returns the block
+    totals of one query. Block j covers keys [j*B, min((j+1)*B, n_kv)).
+    Returns ``m, S`` shaped (B, H, n_q, nblocks) and ``W`` shaped
+    (B, H, n_q, nblocks, dv), natural-log anchors."""
+    _validate(query, key, value)
+    q, k, v = (_prep(_as_4d(t, n)) for t, n in ((query, "query"), (key, "key"), (value, "value")))
+    B, H, n_q, d = q.shape
+    n_kv, dv = k.shape[2], v.shape[-1]
+    block_size = int(block_size)
+    if block_size < 1:
+        raise ShapeError(f"block size must be >= 1, got {block_size}")
+    nb = -(-n_kv // block_size)
+    sc = (1.0 / math.sqrt(d)) if scale is None else float(scale)
+    shp = _shape(q, k, v)
+    m = torch.empty((B, H, n_q, nb), device=q.device, dtype=torch.float32)
+    S = torch.empty_like(m)
+    W = torch.empty((B, H, n_q, nb, dv), device=q.device, dtype=torch.float32)
+    with torch.cuda.device(q.device):
+        st = _lib.lib().elsa_blockwise_f32(
+            ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),
+            ctypes.c_void_p(v.data_ptr()), ctypes.byref(shp), ctypes.c_double(sc),
+            int(block_size), ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(S.data_ptr()),
+            ctypes.c_void_p(W.data_ptr()), _stream_ptr(q.device))
+        _lib.check_status(st, "elsa_blockwise_f32")
+    return m, S, W
+
+
+def inter_block_combine(m, S, W, return_prefixes=False):
+    """The reference's two-pass block combine on the GPU (engine.py:265-297):
+    identity-padded up-sweep to each row's total and, with
+    ``return_prefixes``, the down-sweep's exclusive per-block prefixes
+    (identity first). ``m, S``: (*rows, K); ``W``: (*rows, K, dv), FP32 CUDA,
+    natural-log anchors (the layout :func:`blockwise_states` returns)."""
+    for name, t in (("m", m), ("S", S), ("W", W)):
+        if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_cuda:
+            raise ShapeError(f"{name} must be a float32 CUDA tensor")
+    if m.dim() < 1 or m.shape[-1] < 1:
+        raise ShapeError("no block totals to combine")
+    if tuple(S.shape) != tuple(m.shape) or tuple(W.shape[:-1]) != tuple(m.shape):
+        raise ShapeError("m, S, W shapes disagree")
+    K, dv = m.shape[-1], W.shape[-1]
+    rows_shape = tuple(m.shape[:-1])
+    rows = math.prod(rows_shape) if rows_shape else 1
+    mc, Sc, Wc = m.contiguous(), S.contiguous(), W.contiguous()
+    dev = m.device
+    tm = torch.empty(rows_shape, device=dev, dtype=torch.float32)
+    tS = torch.empty_like(tm)
+    tW = torch.empty((*rows_shape, dv), device=dev, dtype=torch.float32)
+    pre = None
+    if return_prefixes:
+        pre = (torch.empty_like(mc), torch.empty_like(Sc), torch.empty_like(Wc))
+    h = _lib.lib()
+    with torch.cuda.device(dev):
+        ws_bytes = h.elsa_block_scan_workspace_bytes(int(rows), int(K), int(dv))
+        if ws_bytes == 0 and rows > 0:
+            raise ShapeError(f"unsupported block scan geometry (K={K}, dv={dv})")
+        ws = torch.empty(max(ws_bytes, 1), device=dev, dtype=torch.uint8)
+        ptr = (lambda t: ctypes.c_void_p(t.data_ptr()))
+        st = h.elsa_block_scan_f32(
+            ptr(mc), ptr(Sc), ptr(Wc), int(rows), int(K), int(dv), ptr(tm), ptr(tS), ptr(tW),
+            *(ptr(t) for t in pre) if pre else (None, None, None),
+            ptr(ws), ctypes.c_size_t(ws_bytes), _stream_ptr(dev))
+        _lib.check_status(st, "elsa_block_scan_f32")
+    return ((tm, tS, tW), pre) if return_prefixes else (tm, tS, tW)
 
 
 def ffma_peak_tflops(device=None):

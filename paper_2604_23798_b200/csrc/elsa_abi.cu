@@ -22,6 +22,7 @@
 #include "fwd_f32.cuh"
 #include "fwd_tc.cuh"
 #include "merge_f32.cuh"
+#include "block_scan_f32.cuh"
 
 namespace elsa {
 __device__ int g_device_error;
@@ -275,7 +276,7 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
   using T = FwdTraits<W, TK, ST, R>;
   p.qtiles = int(ceil_div(s->n_q, T::TQ));
   const int64_t tiles = ceil_div(int64_t(p.kv_end) - p.kv_begin, TK);
-  p.tiles_per_split = int(ceil_div(tiles, splits));
+  if (p.split_keys == 0) p.split_keys = int(ceil_div(tiles, splits) * TK);
 
   CUtensorMap maps[3];
   std::memset(maps, 0, sizeof(maps));
@@ -368,6 +369,7 @@ void fill_common(FwdParams& p, const float* q, const float* k, const float* v,
   p.c = float(c);
   p.neg = scale < 0 ? 1 : 0;
   p.trace = trace_buffer();
+  p.row_stride = 1;
 }
 
 size_t split_ws_bytes(const elsa_shape* s, const Plan& pl) {
@@ -666,6 +668,108 @@ int elsa_merge_f32(const float* m, const float* S, const float* W, int parts, in
   mp.out_pitch = dv;
   mp.err = dc->err;
   return launch_merge(mp, static_cast<cudaStream_t>(stream));
+}
+
+int elsa_blockwise_f32(const float* q, const float* k, const float* v, const elsa_shape* shp,
+                       double scale, int64_t block_size, float* m, float* S, float* W,
+                       void* stream) {
+  t_last_launches = 0;
+  if (!valid_shape(shp) || block_size < 1 || !std::isfinite(scale)) return ELSA_ERR_SHAPE;
+  if (!q || !k || !v || !m || !S || !W) return ELSA_ERR_SHAPE;
+  if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  int64_t q_st[3], k_st[3], v_st[3];
+  std::memcpy(q_st, shp->q_stride, sizeof(q_st));
+  std::memcpy(k_st, shp->k_stride, sizeof(k_st));
+  std::memcpy(v_st, shp->v_stride, sizeof(v_st));
+  sanitize(q_st, shp->n_q, shp->H, shp->B, shp->d);
+  sanitize(k_st, shp->n_kv, shp->H, shp->B, shp->d);
+  sanitize(v_st, shp->n_kv, shp->H, shp->B, shp->dv);
+  const int64_t BH = shp->B * shp->H;
+  const int64_t nb = ceil_div(shp->n_kv, block_size);
+  const int64_t bsz = block_size < shp->n_kv ? block_size : shp->n_kv;
+  if (bsz >= (int64_t(1) << 30)) return ELSA_ERR_SHAPE;
+  // one split per key block; the kernel's own planner picks the CTA shape for
+  // a single-split problem of one block's length
+  Plan plan = plan_for(shp, bsz, 1, dc->sms);
+  plan.splits = 1;
+  constexpr int64_t kMaxGridY = 65535;
+  for (int64_t b0 = 0; b0 < nb; b0 += kMaxGridY) {
+    const int64_t cnt = nb - b0 < kMaxGridY ? nb - b0 : kMaxGridY;
+    FwdParams p;
+    fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
+    p.kv_begin = int(b0 * block_size);
+    p.kv_end = int(shp->n_kv);
+    p.split_keys = int(bsz);
+    p.err = dc->err;
+    p.bh_begin = 0;
+    p.mode = kModePartialNat;
+    p.pm = m + b0;
+    p.pS = S + b0;
+    p.pW = W + b0 * shp->dv;
+    p.part_stride = 1;
+    p.row_stride = nb;
+    p.pw_pitch = int(shp->dv);
+    p.pw_vec = (reinterpret_cast<uintptr_t>(p.pW) % 16 == 0) && (shp->dv % 4 == 0);
+    Plan pl = plan;
+    pl.splits = int(cnt);
+    if (int st = launch_fwd(p, shp, q_st, k_st, v_st, pl, BH, dc,
+                            static_cast<cudaStream_t>(stream)))
+      return st;
+  }
+  return ELSA_OK;
+}
+
+size_t elsa_block_scan_workspace_bytes(int64_t rows, int nblocks, int dv) {
+  if (rows < 0 || nblocks < 1 || dv < 1 || dv > 64) return 0;
+  int64_t kp = 1;
+  while (kp < nblocks) kp <<= 1;
+  return size_t(rows) * size_t(kp) * size_t(2 + dv) * sizeof(float);
+}
+
+int elsa_block_scan_f32(const float* m, const float* S, const float* W, int64_t rows, int nblocks,
+                        int dv, float* total_m, float* total_S, float* total_W, float* pre_m,
+                        float* pre_S, float* pre_W, void* workspace, size_t ws_bytes,
+                        void* stream) {
+  t_last_launches = 0;
+  if (rows < 0 || nblocks < 1 || dv < 1 || dv > 64) return ELSA_ERR_SHAPE;
+  if (!m || !S || !W || !total_m || !total_S || !total_W) return ELSA_ERR_SHAPE;
+  const bool pre = pre_m || pre_S || pre_W;
+  if (pre && !(pre_m && pre_S && pre_W)) return ELSA_ERR_SHAPE;
+  if (rows == 0) return ELSA_OK;
+  if (!workspace || ws_bytes < elsa_block_scan_workspace_bytes(rows, nblocks, dv))
+    return ELSA_ERR_WORKSPACE;
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  BlockScanParams bp;
+  std::memset(&bp, 0, sizeof(bp));
+  bp.m = m;
+  bp.S = S;
+  bp.W = W;
+  bp.rows = rows;
+  bp.K = nblocks;
+  bp.K_pad = 1;
+  bp.levels = 0;
+  while (bp.K_pad < nblocks) {
+    bp.K_pad <<= 1;
+    ++bp.levels;
+  }
+  bp.dv = dv;
+  bp.ws = static_cast<float*>(workspace);
+  bp.total_m = total_m;
+  bp.total_S = total_S;
+  bp.total_W = total_W;
+  bp.pre_m = pre ? pre_m : nullptr;
+  bp.pre_S = pre_S;
+  bp.pre_W = pre_W;
+  constexpr int kWarps = 8;
+  const int64_t blocks = ceil_div(rows, kWarps);
+  if (blocks >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
+  block_scan_f32_kernel<<<unsigned(blocks), kWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(bp);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "block scan launch");
+  ++t_last_launches;
+  return ELSA_OK;
 }
 
 int elsa_get_device_error(void* stream, int* code) {

@@ -67,14 +67,15 @@ struct FwdParams {
   int neg;  // scale < 0: fold the sign into Q^T
   int kv_begin, kv_end;
   int bh_begin;  // first flattened (b, h) index of this launch (row batching)
-  int tiles_per_split;
+  int split_keys;  // keys per split: split s covers [kv_begin + s*split_keys, +split_keys) ∩ [.., kv_end)
   int qtiles;
   int mode;
   int y_vec;  // float4 stores to Y legal
   float* pm;
   float* pS;
   float* pW;
-  int64_t part_stride;  // rows per split in the partial buffers
+  int64_t part_stride;  // state slots between consecutive splits in the partial buffers
+  int64_t row_stride;   // state slots between consecutive rows (1, or nblocks for blockwise)
   int pw_pitch;         // floats per row of pW
   int pw_vec;           // float4 stores to pW legal
   int* err;
@@ -181,7 +182,7 @@ template <class T>
 __device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw, float* Ks,
                                                  float* Vs, uint64_t* full, uint64_t* empty,
                                                  uint64_t* qbar, int b, int h, int q0,
-                                                 int t_begin, int ntiles, int lane) {
+                                                 int split_lo, int ntiles, int lane) {
   // Plain-load fallback for operands TMA cannot describe (misaligned base or
   // strides, zero strides). Same smem layout as the TMA boxes, zero-filled.
   const float* qg = p.q + int64_t(b) * p.qs_b + int64_t(h) * p.qs_h;
@@ -199,7 +200,7 @@ __device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % T::STAGES;
     if (t >= T::STAGES) ptx::mbar_wait(&empty[s], ((t / T::STAGES) - 1) & 1);
-    const int key0 = p.kv_begin + (t_begin + t) * T::TK;
+    const int key0 = split_lo + t * T::TK;
     float* ks = Ks + s * T::K_FLOATS;
     float* vs = Vs + s * T::V_FLOATS;
     for (int idx = lane; idx < T::K_FLOATS; idx += 32) {
@@ -255,11 +256,10 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
   const int h = bh - b * p.H;
   const int q0 = qtile * T::TQ;
 
-  const int ntiles_total = (p.kv_end - p.kv_begin + TK - 1) / TK;
-  const int t_begin = split * p.tiles_per_split;
-  const int t_end = min(t_begin + p.tiles_per_split, ntiles_total);
-  const int ntiles = max(t_end - t_begin, 0);
-  const int kv_hi = min(p.kv_end, p.kv_begin + t_end * TK);
+  const int64_t lo64 = int64_t(p.kv_begin) + int64_t(split) * p.split_keys;
+  const int split_lo = int(lo64 < p.kv_end ? lo64 : p.kv_end);
+  const int kv_hi = int(lo64 + p.split_keys < p.kv_end ? lo64 + p.split_keys : p.kv_end);
+  const int ntiles = kv_hi > split_lo ? (kv_hi - split_lo + TK - 1) / TK : 0;
 
   trace_cta(p, 0);
   if (threadIdx.x == 0) {
@@ -288,14 +288,14 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
         for (int t = 0; t < ntiles; ++t) {
           const int s = t % T::STAGES;
           if (t >= T::STAGES) ptx::mbar_wait(&empty[s], ((t / T::STAGES) - 1) & 1);
-          const int key0 = p.kv_begin + (t_begin + t) * TK;
+          const int key0 = split_lo + t * TK;
           ptx::mbar_arrive_expect_tx(&full[s], T::KV_TX_BYTES);
           ptx::tma_load_4d(Ks + s * T::K_FLOATS, &tmK, &full[s], 0, key0, h, b);
           ptx::tma_load_4d(Vs + s * T::V_FLOATS, &tmV, &full[s], 0, key0, h, b);
         }
       }
     } else {
-      producer_generic<T>(p, Qraw, Ks, Vs, full, empty, qbar, b, h, q0, t_begin, ntiles, lane);
+      producer_generic<T>(p, Qraw, Ks, Vs, full, empty, qbar, b, h, q0, split_lo, ntiles, lane);
     }
     return;
   }
@@ -427,7 +427,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
     trace_mark(p, warp, t, 2);
 
     // ---- mask keys past this split's range ----
-    const int key0 = p.kv_begin + (t_begin + t) * TK;
+    const int key0 = split_lo + t * TK;
     if (key0 + TK > kv_hi) {
 #pragma unroll
       for (int j = 0; j < RK; ++j)
@@ -527,7 +527,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
         }
       } else {
         const int64_t row = int64_t(bh_rel) * p.n_q + qrow;  // relative to this batch
-        const int64_t idx = int64_t(split) * p.part_stride + row;
+        const int64_t idx = int64_t(split) * p.part_stride + row * p.row_stride;
         if (g == 0) {
           const float m = (p.mode == kModePartialNat) ? mrow[i] * 0.69314718055994531f : mrow[i];
           p.pm[idx] = m;

@@ -22,3 +22,27 @@ class ElsaCudaError(RuntimeError):
 
 class ElsaLibraryError(ImportError):
     """libelsa.so is missing or unloadable; there is no CPU fallback."""
+
+
+class TensorFileError(Exception):
+    """ATN1 tensor-file format violation (errors.py:32)."""
+
+
+class BadMagicError(TensorFileError):
+    """Not an ATN1 file (errors.py:36)."""
+
+
+class BadVersionError(TensorFileError):
+    """Unsupported ATN1 version (errors.py:40)."""
+
+
+class BadDtypeError(TensorFileError):
+    """Unknown ATN1 dtype code (errors.py:44)."""
+
+
+class TruncatedPayloadError(TensorFileError):
+    """Payload shorter than the header promises, or bad trailer (errors.py:48)."""
+
+
+class DimsMismatchError(TensorFileError):
+    """Payload length disagrees with the dims (errors.py:53)."""

@@ -32,6 +32,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import attention as _att
 from .attention import resolve_kv_splits, scaled_dot_product_attention
 from .errors import ShapeError
 
@@ -45,6 +46,12 @@ __all__ = [
     "scan_depth",
     "depth_cap",
     "scan_forward",
+    "analytic_trace",
+    "StateTriple",
+    "blockwise_states",
+    "inter_block_combine",
+    "block_validation",
+    "BlockValidationReport",
 ]
 
 
@@ -202,6 +209,27 @@ def _precision_name(p):
     return getattr(p, "value", str(p)).lower()
 
 
+def analytic_trace(b, h, n, block_size, splits, workspace_bytes=None):
+    """ScanTrace of the GPU schedule for a (b, h, n) problem run with
+    ``splits`` KV splits (see :class:`ScanTrace`); ``workspace_bytes`` is the
+    split workspace the library asked for (elsa_workspace_bytes), else the
+    unbatched size."""
+    tiles = -(-n // KEY_TILE)
+    tps = -(-tiles // splits)
+    paths = b * h * n
+    return ScanTrace(
+        merge_count=paths * (tiles + splits - 1),
+        critical_depth=scan_depth(n, block_size),
+        per_level_counts=[paths * tiles] + ([paths * (splits - 1)] if splits > 1 else []),
+        leaf_count=b * h * n * n,
+        peak_extra_memory=(int(workspace_bytes) if workspace_bytes is not None
+                           else (splits * b * h * n * (2 + 64) * 4) if splits > 1 else 0),
+        n_paths=paths,
+        schedule_depth=4 + tps + _clog2(splits),
+        kv_splits=splits,
+    )
+
+
 def scan_forward(problem, cfg=None, device=None):
     """GPU ``scan_forward``: returns ``(AttentionOutput, ScanTrace | None)``."""
     cfg = ScanConfig() if cfg is None else cfg
@@ -230,18 +258,148 @@ def scan_forward(problem, cfg=None, device=None):
     out = AttentionOutput(y_t4)
     trace = None
     if getattr(cfg, "trace", False):
-        splits = resolve_kv_splits(q, k, v, splits_req)
-        tiles = -(-n // KEY_TILE)
-        tps = -(-tiles // splits)
-        paths = b * h * n
-        trace = ScanTrace(
-            merge_count=paths * (tiles + splits - 1),
-            critical_depth=scan_depth(n, cfg.block_size),
-            per_level_counts=[paths * tiles] + ([paths * (splits - 1)] if splits > 1 else []),
-            leaf_count=b * h * n * n,
-            peak_extra_memory=(splits * b * h * n * (2 + 64) * 4) if splits > 1 else 0,
-            n_paths=paths,
-            schedule_depth=4 + tps + _clog2(splits),
-            kv_splits=splits,
-        )
+        trace = analytic_trace(b, h, n, cfg.block_size, resolve_kv_splits(q, k, v, splits_req),
+                               _att.workspace_bytes(q, k, v, splits_req))
     return out, trace
+
+
+# ---------------------------------------------------------------------------
+# Block-level surface: engine.blockwise_states,
+# engine.inter_block_combine and verify.block_validation on device states.
+
+
+@dataclass(frozen=True)
+class StateTriple:
+    """(m, S, W) summary of one key range (monoid.py:73-120), host copy."""
+
+    m: float
+    S: float
+    W: np.ndarray
+
+    def is_identity(self):
+        return bool(np.isneginf(self.m))
+
+
+def _triples(m, S, W):
+    return [StateTriple(np.float32(a), np.float32(b), np.asarray(c, dtype=np.float32))
+            for a, b, c in zip(m, S, W)]
+
+
+def _problem_tensors(problem, dev):
+    return tuple(torch.from_numpy(np.ascontiguousarray(t.data, dtype=np.float32)).to(dev)
+                 for t in (problem.Q, problem.K, problem.V))
+
+
+def blockwise_states(problem, cfg, query_index, b_idx=0, h_idx=0, block_size=None, device=None):
+    """Per-block totals for one query (engine.py:430-451), computed by the
+    sm_100a blockwise kernel (elsa_blockwise_f32). ``block_size`` overrides
+    ``cfg.block_size``; returns a list of :class:`StateTriple`."""
+    B = cfg.block_size if block_size is None else int(block_size)
+    if B < 1:
+        raise ShapeError(f"block size must be >= 1, got {B}")
+    b, h, n, d = problem.Q.data.shape
+    if not (0 <= query_index < n):
+        raise ShapeError(f"query index {query_index} out of range [0, {n})")
+    if _precision_name(getattr(cfg, "precision", Precision.FP32)) != "fp32":
+        raise ShapeError("the GPU block path computes in FP32 only")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    q, k, v = _problem_tensors(problem, dev)
+    qi = q[b_idx:b_idx + 1, h_idx:h_idx + 1, query_index:query_index + 1]
+    m, S, W = _att.blockwise_states(qi, k[b_idx:b_idx + 1, h_idx:h_idx + 1],
+                                    v[b_idx:b_idx + 1, h_idx:h_idx + 1], block_size=B,
+                                    scale=float(problem.scale))
+    return _triples(m[0, 0, 0].cpu().numpy(), S[0, 0, 0].cpu().numpy(), W[0, 0, 0].cpu().numpy())
+
+
+def inter_block_combine(block_totals, return_prefixes=False, device=None):
+    """engine.py:265-297 on the device: the up-sweep total and, optionally,
+    the exclusive prefixes (identity first)."""
+    totals = list(block_totals)
+    if not totals:
+        raise ShapeError("no block totals to combine")
+    widths = {np.asarray(t.W).shape[0] for t in totals}
+    if len(widths) != 1:
+        raise ShapeError(f"mixed value widths {sorted(widths)}")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    m = torch.tensor([[float(t.m) for t in totals]], dtype=torch.float32, device=dev)
+    S = torch.tensor([[float(t.S) for t in totals]], dtype=torch.float32, device=dev)
+    W = torch.from_numpy(np.stack([np.asarray(t.W, dtype=np.float32) for t in totals])[None]).to(dev)
+    res = _att.inter_block_combine(m, S, W, return_prefixes=return_prefixes)
+    (tm, tS, tW), pre = (res if return_prefixes else (res, None))
+    total = StateTriple(np.float32(tm[0].item()), np.float32(tS[0].item()), tW[0].cpu().numpy())
+    if not return_prefixes:
+        return total
+    return total, _triples(pre[0][0].cpu().numpy(), pre[1][0].cpu().numpy(), pre[2][0].cpu().numpy())
+
+
+def _triple_rel_dev(t1, t2):
+    """verify.py:218-227."""
+    tiny = np.finfo(np.float64).tiny
+    def parts(t):
+        W = np.asarray(t.W, dtype=np.float64)
+        return np.concatenate([[float(t.m)], [float(t.S)], W, W / max(float(t.S), tiny)])
+    p1, p2 = parts(t1), parts(t2)
+    denom = np.maximum(np.maximum(np.abs(p1), np.abs(p2)), tiny)
+    return float(np.max(np.abs(p1 - p2) / denom))
+
+
+@dataclass
+class BlockValidationReport:
+    """verify.py:230-246."""
+
+    partitions: list
+    query_points: list
+    max_pairwise_dev: float
+    max_vs_sequential_dev: float
+    per_partition_dev: dict
+
+    def passed(self, tol):
+        return self.max_pairwise_dev <= tol and self.max_vs_sequential_dev <= tol
+
+    def to_dict(self):
+        return {
+            "partitions": list(self.partitions),
+            "query_points": [list(q) for q in self.query_points],
+            "max_pairwise_dev": self.max_pairwise_dev,
+            "max_vs_sequential_dev": self.max_vs_sequential_dev,
+            "per_partition_dev": {str(k): v for k, v in self.per_partition_dev.items()},
+        }
+
+
+def block_validation(problem, cfg, partitions, query_indices=None, device=None):
+    """verify.block_validation (verify.py:249-282) on device states: for each
+    partition size the per-block states of every query come from
+    elsa_blockwise_f32 and their totals from the device up-sweep
+    (elsa_block_scan_f32); totals are compared pairwise and against the
+    whole-range single-chain state (elsa_partial_f32 with one split, the GPU
+    path's own left-to-right fold, standing in for the reference's per-key
+    sequential fold)."""
+    partitions = [int(p) for p in partitions]
+    if any(p < 1 for p in partitions):
+        raise ShapeError("partition block sizes must be >= 1")
+    b, h, n, d = problem.Q.data.shape
+    if query_indices is None:
+        query_indices = sorted({0, n // 3, (2 * n) // 3, n - 1})
+    heads = sorted({(0, 0), (b - 1, h - 1)})
+    points = [(bi, hi, qi) for (bi, hi) in heads for qi in query_indices]
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    q, k, v = _problem_tensors(problem, dev)
+    sc = float(problem.scale)
+    seq_m, seq_S, seq_W = _att.partial_states(q, k, v, scale=sc, kv_splits=1)
+    totals_by_p = {}
+    for p in partitions:
+        m, S, W = _att.blockwise_states(q, k, v, block_size=p, scale=sc)
+        totals_by_p[p] = tuple(t.cpu().numpy() for t in _att.inter_block_combine(m, S, W))
+    max_pair = max_seq = 0.0
+    per_partition = {p: 0.0 for p in partitions}
+    for bi, hi, qi in points:
+        seq = StateTriple(seq_m[bi, hi, qi].item(), seq_S[bi, hi, qi].item(),
+                          seq_W[bi, hi, qi].cpu().numpy())
+        tot = [StateTriple(*(a[bi, hi, qi] for a in totals_by_p[p])) for p in partitions]
+        for i, t1 in enumerate(tot):
+            dev_ = _triple_rel_dev(t1, seq)
+            max_seq = max(max_seq, dev_)
+            per_partition[partitions[i]] = max(per_partition[partitions[i]], dev_)
+            for t2 in tot[i + 1:]:
+                max_pair = max(max_pair, _triple_rel_dev(t1, t2))
+    return BlockValidationReport(partitions, points, max_pair, max_seq, per_partition)

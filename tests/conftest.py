@@ -23,7 +23,7 @@ def load_golden(name):
 
 @pytest.fixture(scope="session")
 def golden():
-    return {n: load_golden(n + ".npz") for n in ("generator", "depth", "monoid", "attention")}
+    return {n: load_golden(n + ".npz") for n in ("generator", "depth", "monoid", "attention", "blocks", "harness")}
 
 
 SCEN = ["regular", "long", "stress"]
