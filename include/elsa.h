@@ -17,6 +17,8 @@
  *                        (score-tile producer engine.py:352-358, intra-block
  *                        scan engine.py:148-176/315-339, inter-block sweep
  *                        engine.py:179-199, epilogue engine.py:375-382)
+ *   elsa_fwd_f32_host <- the same call with the reference's host (numpy)
+ *                        arrays in and out, copies pipelined with the kernels
  *   elsa_partial_f32  <- engine.blockwise_states(...) + inter_block_combine
  *                        engine.py:430-451 / 265-297: the (m, S, W) summary
  *                        of one contiguous key range (Proposition 1,
@@ -88,6 +90,25 @@ size_t elsa_workspace_bytes(const elsa_shape* shp, int kv_splits);
 int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
                  const elsa_shape* shp, double scale, int kv_splits,
                  void* workspace, size_t ws_bytes, void* stream);
+
+/* Device workspace elsa_fwd_f32_host needs: device copies of Q, K, V and Y
+ * plus the kv-split workspace of each concurrently running head group. */
+size_t elsa_host_workspace_bytes(const elsa_shape* shp, int kv_splits);
+
+/* Y = softmax(Q K^T * scale) V with q, k, v, y in HOST memory (dense
+ * row-major (B,H,n,d) arrays; the shape's strides must describe that dense
+ * layout). The reference's entry point takes host arrays
+ * (engine.scan_forward, engine.py:385-427: numpy in, a new numpy Y out); this
+ * is its end-to-end counterpart: the (b, h) heads are cut into groups whose
+ * host->device copies, forward kernels and device->host copies overlap on
+ * internal per-device streams, all ordered after prior work on `stream`;
+ * `stream` waits for the last copy, so y is complete once `stream` is.
+ * Page-locked host buffers make the copies asynchronous; pageable ones work
+ * but serialise the host. dev_workspace: elsa_host_workspace_bytes() bytes of
+ * device memory. Same status codes and device error word as elsa_fwd_f32. */
+int elsa_fwd_f32_host(const float* q, const float* k, const float* v, float* y,
+                      const elsa_shape* shp, double scale, int kv_splits,
+                      void* dev_workspace, size_t ws_bytes, void* stream);
 
 /* Partial state of keys [kv_begin, kv_end) for every query row:
  * m[row] (natural-log anchor, -inf for an empty range), S[row], and

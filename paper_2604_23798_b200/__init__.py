@@ -6,6 +6,8 @@ Entry points:
   * scaled_dot_product_attention(q, k, v) — drop-in for
     torch.nn.functional.scaled_dot_product_attention on (B, H, n, d) FP32
     CUDA tensors;
+  * attention_from_host(q, k, v) — the same on HOST arrays, with the
+    host<->device copies pipelined under the kernels (elsa_fwd_f32_host);
   * partial_states / merge_states — per-key-range (m, S, W) summaries and
     their fixed (+)-tree merge (Proposition 1), the building blocks of the
     KV-sharded multi-GPU path in ``paper_2604_23798_b200.dist``;
@@ -14,6 +16,7 @@ Entry points:
 """
 
 from .attention import (  # noqa: F401
+    attention_from_host,
     blockwise_states,
     inter_block_combine,
     check_device_error,

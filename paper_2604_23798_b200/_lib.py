@@ -27,6 +27,8 @@ EXPORTED_SYMBOLS = (
     "elsa_resolve_kv_splits",
     "elsa_workspace_bytes",
     "elsa_fwd_f32",
+    "elsa_host_workspace_bytes",
+    "elsa_fwd_f32_host",
     "elsa_partial_f32",
     "elsa_fwd_f16",
     "elsa_merge_f32",
@@ -87,6 +89,10 @@ def _declare(h):
     h.elsa_workspace_bytes.argtypes = [shp, c_int]
     h.elsa_fwd_f32.restype = c_int
     h.elsa_fwd_f32.argtypes = [c_vp, c_vp, c_vp, c_vp, shp, c_dbl, c_int, c_vp, c_sz, c_vp]
+    h.elsa_host_workspace_bytes.restype = c_sz
+    h.elsa_host_workspace_bytes.argtypes = [shp, c_int]
+    h.elsa_fwd_f32_host.restype = c_int
+    h.elsa_fwd_f32_host.argtypes = [c_vp, c_vp, c_vp, c_vp, shp, c_dbl, c_int, c_vp, c_sz, c_vp]
     h.elsa_partial_f32.restype = c_int
     h.elsa_partial_f32.argtypes = [c_vp, c_vp, c_vp, shp, c_dbl, c_i64, c_i64,
                                    c_vp, c_vp, c_vp, c_int, c_vp, c_sz, c_vp]

@@ -26,6 +26,7 @@ from .errors import NumericalError, ShapeError
 
 __all__ = [
     "scaled_dot_product_attention",
+    "attention_from_host",
     "partial_states",
     "merge_states",
     "blockwise_states",
@@ -125,11 +126,16 @@ def check_device_error(device=None):
         _lib.check_status(code.value, "device")
 
 
+def _plan_device(t):
+    # planning only reads shapes and strides; host tensors plan for the current device
+    return t.device if t.is_cuda else torch.device("cuda", torch.cuda.current_device())
+
+
 def resolve_kv_splits(q, k, v, kv_splits=0):
     """Split count elsa_fwd_f32 uses for these shapes (0 = auto)."""
     q4, k4, v4 = _as_4d(q, "query"), _as_4d(k, "key"), _as_4d(v, "value")
     shp = _shape(q4, k4, v4)
-    with torch.cuda.device(q4.device):
+    with torch.cuda.device(_plan_device(q4)):
         r = _lib.lib().elsa_resolve_kv_splits(ctypes.byref(shp), int(kv_splits))
     if r < 0:
         _lib.check_status(-r, "elsa_resolve_kv_splits")
@@ -140,7 +146,7 @@ def workspace_bytes(q, k, v, kv_splits=0):
     """Split workspace elsa_fwd_f32 needs for these shapes (0 = none)."""
     q4, k4, v4 = _as_4d(q, "query"), _as_4d(k, "key"), _as_4d(v, "value")
     shp = _shape(q4, k4, v4)
-    with torch.cuda.device(q4.device):
+    with torch.cuda.device(_plan_device(q4)):
         return int(_lib.lib().elsa_workspace_bytes(ctypes.byref(shp), int(kv_splits)))
 
 
@@ -149,7 +155,7 @@ def describe_plan(q, k, v, kv_splits=0):
     q4, k4, v4 = _as_4d(q, "query"), _as_4d(k, "key"), _as_4d(v, "value")
     shp = _shape(q4, k4, v4)
     buf = ctypes.create_string_buffer(128)
-    with torch.cuda.device(q4.device):
+    with torch.cuda.device(_plan_device(q4)):
         _lib.check_status(_lib.lib().elsa_describe_plan(ctypes.byref(shp), int(kv_splits), buf, 128),
                           "elsa_describe_plan")
     return buf.value.decode()
@@ -216,6 +222,84 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
         if check_numerics:
             check_device_error(q.device)
     if orig_dim == 4 or out is not None:
+        return y
+    return y.reshape(*orig_shape[:-1], dv)
+
+
+_HOST_WS = {}
+
+
+def _host_workspace(device, nbytes):
+    """Device workspace of the host pipeline, kept per device and grown on
+    demand (the library itself never allocates)."""
+    ws = _HOST_WS.get(device.index)
+    if ws is None or ws.numel() < nbytes:
+        _HOST_WS.pop(device.index, None)
+        ws = torch.empty(max(nbytes, 1), device=device, dtype=torch.uint8)
+        _HOST_WS[device.index] = ws
+    return ws
+
+
+def _host_tensor(x, name):
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        import numpy as np
+        t = torch.from_numpy(np.ascontiguousarray(x))
+    if t.is_cuda:
+        raise ShapeError(f"{name} is already on {t.device}: use scaled_dot_product_attention")
+    if t.dtype != torch.float32:
+        raise ShapeError(f"{name} dtype {t.dtype}: the host pipeline takes float32 only")
+    return t.contiguous()
+
+
+def attention_from_host(query, key, value, scale=None, *, out=None, kv_splits=0, device=None,
+                        check_numerics=False, sync=True):
+    """Exact FP32 attention on HOST (B, H, n, d) arrays computed on the GPU —
+    the end-to-end form of the reference's ``scan_forward``, which takes and
+    returns host arrays (engine.py:385-427).
+
+    ``elsa_fwd_f32_host`` cuts the (b, h) heads into groups and overlaps each
+    group's host->device copies, its forward kernels and its device->host copy
+    on internal streams, ordered after prior work on the current stream.
+    Page-locked inputs and ``out`` (``tensor.pin_memory()``) make the copies
+    asynchronous. Returns ``out`` (a new CPU tensor if None); with ``sync``
+    the call returns once Y is on the host, otherwise Y is complete when the
+    current stream reaches this point."""
+    q, k, v = (_host_tensor(t, n) for t, n in ((query, "query"), (key, "key"), (value, "value")))
+    orig_shape = q.shape
+    q, k, v = (_as_4d(t, n).contiguous() for t, n in ((q, "query"), (k, "key"), (v, "value")))
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else \
+        torch.device(device)
+    d = q.shape[-1]
+    sc = (1.0 / math.sqrt(d)) if scale is None else float(scale)
+    if not math.isfinite(sc):
+        raise ShapeError(f"scale must be finite, got {sc}")
+    B, H, n_q, _ = q.shape
+    dv = v.shape[-1]
+    if out is None:
+        y = torch.empty((B, H, n_q, dv), dtype=torch.float32, pin_memory=q.is_pinned())
+    else:
+        y = out
+        if tuple(y.shape) != (B, H, n_q, dv) or y.dtype != torch.float32 or y.is_cuda \
+                or not y.is_contiguous():
+            raise ShapeError("out must be a contiguous float32 (B, H, n_q, dv) host tensor")
+    shp = _shape(q, k, v, y)
+    h = _lib.lib()
+    with torch.cuda.device(dev):
+        ws_bytes = h.elsa_host_workspace_bytes(ctypes.byref(shp), int(kv_splits))
+        ws = _host_workspace(dev, ws_bytes)
+        st = h.elsa_fwd_f32_host(
+            ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),
+            ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(y.data_ptr()), ctypes.byref(shp),
+            ctypes.c_double(sc), int(kv_splits), ctypes.c_void_p(ws.data_ptr()),
+            ctypes.c_size_t(ws_bytes), _stream_ptr(dev))
+        _lib.check_status(st, "elsa_fwd_f32_host")
+        if check_numerics:
+            check_device_error(dev)
+        elif sync:
+            torch.cuda.current_stream(dev).synchronize()
+    if out is not None or len(orig_shape) == 4:
         return y
     return y.reshape(*orig_shape[:-1], dv)
 

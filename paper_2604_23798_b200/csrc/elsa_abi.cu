@@ -407,7 +407,7 @@ bool aligned16(const void* ptr, const int64_t st[3]) {
 int run_forward(const float* q, const float* k, const float* v, const elsa_shape* shp,
                 double scale, int64_t kv_begin, int64_t kv_end, int kv_splits, void* workspace,
                 size_t ws_bytes, cudaStream_t strm, float* y, float* m_out, float* S_out,
-                float* W_out) {
+                float* W_out, const Plan* force_plan = nullptr) {
   DeviceCache* dc = nullptr;
   if (int st = current_device_cache(&dc)) return st;
   int64_t q_st[3], k_st[3], v_st[3];
@@ -420,7 +420,9 @@ int run_forward(const float* q, const float* k, const float* v, const elsa_shape
 
   const int64_t BH = shp->B * shp->H;
   const int64_t len = kv_end - kv_begin;
-  const Plan plan = len == 0 ? Plan{kCfgW4R8, 1, BH} : plan_for(shp, len, kv_splits, dc->sms);
+  const Plan plan = len == 0        ? Plan{kCfgW4R8, 1, BH}
+                    : force_plan ? *force_plan
+                                 : plan_for(shp, len, kv_splits, dc->sms);
   const bool final_out = y != nullptr;
   FwdParams p;
   fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
@@ -501,6 +503,113 @@ int run_forward(const float* q, const float* k, const float* v, const elsa_shape
   return ELSA_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Host-buffer pipeline (elsa_fwd_f32_host). The (b, h) heads are cut into up
+// to kPipeMaxGroups groups; group g's Q/K/V go host -> device on one copy
+// stream, its forward runs on compute stream g % kPipeStreams as soon as its
+// inputs landed, and its Y goes device -> host on a second copy stream as soon
+// as it is computed. Several compute streams keep CTAs of the next groups
+// resident while a group drains, so the device runs the same plan (config and
+// kv splits of the WHOLE problem) at the same occupancy as one launch, and the
+// PCIe transfers hide under the FFMA work except for the first group's inputs
+// and the last group's output.
+// ---------------------------------------------------------------------------
+constexpr int kPipeStreams = 4;
+constexpr int kPipeMaxGroups = 16;
+
+struct HostPipe {
+  bool ready = false;
+  cudaStream_t in = nullptr, out = nullptr, comp[kPipeStreams] = {};
+  cudaEvent_t start = nullptr, done = nullptr;
+  cudaEvent_t ev_in[kPipeMaxGroups] = {}, ev_comp[kPipeMaxGroups] = {};
+  std::mutex mu;  // one enqueue sequence at a time per device (events are reused)
+};
+HostPipe g_pipe[kMaxDevices];
+
+int host_pipe(HostPipe** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return ELSA_ERR_CUDA;
+  HostPipe& hp = g_pipe[dev];
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!hp.ready) {
+    cudaError_t e = cudaStreamCreateWithFlags(&hp.in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&hp.out, cudaStreamNonBlocking);
+    for (int i = 0; i < kPipeStreams && e == cudaSuccess; ++i)
+      e = cudaStreamCreateWithFlags(&hp.comp[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp.start, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp.done, cudaEventDisableTiming);
+    for (int i = 0; i < kPipeMaxGroups && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&hp.ev_in[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp.ev_comp[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "host pipeline streams/events");
+    hp.ready = true;
+  }
+  *out = &hp;
+  return ELSA_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct HostLayout {
+  Plan plan;        // the whole problem's plan, applied to every group
+  Plan group_plan;  // same config / splits, heads_per_batch capped at the group size
+  int64_t hpg = 1;  // (b, h) heads per group
+  int groups = 1;
+  size_t off_k = 0, off_v = 0, off_y = 0, off_ws = 0, ws_each = 0, total = 0;
+};
+
+bool dense_shape(const elsa_shape* s) {
+  const int64_t q[3] = {s->H * s->n_q * s->d, s->n_q * s->d, s->d};
+  const int64_t k[3] = {s->H * s->n_kv * s->d, s->n_kv * s->d, s->d};
+  const int64_t v[3] = {s->H * s->n_kv * s->dv, s->n_kv * s->dv, s->dv};
+  const int64_t y[3] = {s->H * s->n_q * s->dv, s->n_q * s->dv, s->dv};
+  for (int i = 0; i < 3; ++i) {
+    // strides of size-1 axes are irrelevant
+    const bool skip = (i == 0 && s->B == 1) || (i == 1 && s->H == 1);
+    if (skip) continue;
+    if (s->q_stride[i] != q[i] || s->k_stride[i] != k[i] || s->v_stride[i] != v[i] ||
+        s->y_stride[i] != y[i])
+      return false;
+  }
+  return true;
+}
+
+elsa_shape group_shape(const elsa_shape* s, int64_t cnt) {
+  elsa_shape g = *s;
+  g.B = 1;
+  g.H = cnt;
+  const int64_t qs[3] = {cnt * s->n_q * s->d, s->n_q * s->d, s->d};
+  const int64_t ks[3] = {cnt * s->n_kv * s->d, s->n_kv * s->d, s->d};
+  const int64_t vs[3] = {cnt * s->n_kv * s->dv, s->n_kv * s->dv, s->dv};
+  const int64_t ys[3] = {cnt * s->n_q * s->dv, s->n_q * s->dv, s->dv};
+  std::memcpy(g.q_stride, qs, sizeof(qs));
+  std::memcpy(g.k_stride, ks, sizeof(ks));
+  std::memcpy(g.v_stride, vs, sizeof(vs));
+  std::memcpy(g.y_stride, ys, sizeof(ys));
+  return g;
+}
+
+HostLayout host_layout(const elsa_shape* s, int kv_splits, int sms) {
+  HostLayout L;
+  const int64_t BH = s->B * s->H;
+  L.plan = plan_for(s, s->n_kv, kv_splits, sms);
+  const int64_t g = BH < kPipeMaxGroups ? (BH > 0 ? BH : 1) : kPipeMaxGroups;
+  L.hpg = ceil_div(BH > 0 ? BH : 1, g);
+  L.groups = int(ceil_div(BH > 0 ? BH : 1, L.hpg));
+  L.group_plan = L.plan;
+  if (L.group_plan.heads_per_batch > L.hpg) L.group_plan.heads_per_batch = L.hpg;
+  const elsa_shape gs = group_shape(s, L.hpg);
+  L.ws_each = align256(split_ws_bytes(&gs, L.group_plan));
+  const size_t nq = size_t(BH) * size_t(s->n_q), nkv = size_t(BH) * size_t(s->n_kv);
+  L.off_k = align256(nq * size_t(s->d) * 4);
+  L.off_v = L.off_k + align256(nkv * size_t(s->d) * 4);
+  L.off_y = L.off_v + align256(nkv * size_t(s->dv) * 4);
+  L.off_ws = L.off_y + align256(nq * size_t(s->dv) * 4);
+  L.total = L.off_ws + size_t(kPipeStreams) * L.ws_each;
+  return L;
+}
+
 }  // namespace
 
 extern "C" {
@@ -564,6 +673,82 @@ int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
   if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
   return run_forward(q, k, v, shp, scale, 0, shp->n_kv, kv_splits, workspace, ws_bytes,
                      static_cast<cudaStream_t>(stream), y, nullptr, nullptr, nullptr);
+}
+
+size_t elsa_host_workspace_bytes(const elsa_shape* shp, int kv_splits) {
+  if (!valid_shape(shp) || kv_splits < 0) return 0;
+  DeviceCache* dc = nullptr;
+  int sms = 148;
+  if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
+  return host_layout(shp, kv_splits, sms).total;
+}
+
+int elsa_fwd_f32_host(const float* q, const float* k, const float* v, float* y,
+                      const elsa_shape* shp, double scale, int kv_splits, void* dev_workspace,
+                      size_t ws_bytes, void* stream) {
+  t_last_launches = 0;
+  if (!valid_shape(shp) || kv_splits < 0 || !std::isfinite(scale)) return ELSA_ERR_SHAPE;
+  if (!q || !k || !v || !y || !dense_shape(shp)) return ELSA_ERR_SHAPE;
+  if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  const HostLayout L = host_layout(shp, kv_splits, dc->sms);
+  if (!dev_workspace || ws_bytes < L.total) return ELSA_ERR_WORKSPACE;
+  HostPipe* hp = nullptr;
+  if (int st = host_pipe(&hp)) return st;
+  std::lock_guard<std::mutex> lk(hp->mu);
+
+  char* base = static_cast<char*>(dev_workspace);
+  float* dq = reinterpret_cast<float*>(base);
+  float* dk = reinterpret_cast<float*>(base + L.off_k);
+  float* dv = reinterpret_cast<float*>(base + L.off_v);
+  float* dy = reinterpret_cast<float*>(base + L.off_y);
+  const cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  const int64_t BH = shp->B * shp->H;
+  const int64_t nq = shp->n_q, nkv = shp->n_kv, d = shp->d, dvw = shp->dv;
+  int launches = 0;
+  auto fail = [&](cudaError_t e, const char* where) { return cuda_fail(e, where); };
+
+  cudaError_t e = cudaEventRecord(hp->start, caller);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(hp->in, hp->start, 0);
+  if (e != cudaSuccess) return fail(e, "host pipeline start");
+  for (int g = 0; g < L.groups; ++g) {
+    const int64_t bh0 = int64_t(g) * L.hpg;
+    const int64_t cnt = BH - bh0 < L.hpg ? BH - bh0 : L.hpg;
+    const size_t qo = size_t(bh0 * nq * d), ko = size_t(bh0 * nkv * d);
+    const size_t vo = size_t(bh0 * nkv * dvw), yo = size_t(bh0 * nq * dvw);
+    e = cudaMemcpyAsync(dq + qo, q + qo, size_t(cnt * nq * d) * 4, cudaMemcpyHostToDevice, hp->in);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(dk + ko, k + ko, size_t(cnt * nkv * d) * 4, cudaMemcpyHostToDevice,
+                          hp->in);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(dv + vo, v + vo, size_t(cnt * nkv * dvw) * 4, cudaMemcpyHostToDevice,
+                          hp->in);
+    if (e == cudaSuccess) e = cudaEventRecord(hp->ev_in[g], hp->in);
+    const cudaStream_t cs = hp->comp[g % kPipeStreams];
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, hp->ev_in[g], 0);
+    if (e != cudaSuccess) return fail(e, "host pipeline H2D");
+    const elsa_shape gs = group_shape(shp, cnt);
+    Plan gp = L.group_plan;
+    if (gp.heads_per_batch > cnt) gp.heads_per_batch = cnt;
+    void* ws = L.ws_each ? base + L.off_ws + size_t(g % kPipeStreams) * L.ws_each : nullptr;
+    if (int st = run_forward(dq + qo, dk + ko, dv + vo, &gs, scale, 0, nkv, gp.splits, ws,
+                             L.ws_each, cs, dy + yo, nullptr, nullptr, nullptr, &gp))
+      return st;
+    launches += t_last_launches;
+    t_last_launches = 0;
+    e = cudaEventRecord(hp->ev_comp[g], cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hp->out, hp->ev_comp[g], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(y + yo, dy + yo, size_t(cnt * nq * dvw) * 4, cudaMemcpyDeviceToHost,
+                          hp->out);
+    if (e != cudaSuccess) return fail(e, "host pipeline D2H");
+  }
+  e = cudaEventRecord(hp->done, hp->out);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(caller, hp->done, 0);
+  if (e != cudaSuccess) return fail(e, "host pipeline join");
+  t_last_launches = launches;
+  return ELSA_OK;
 }
 
 int elsa_partial_f32(const float* q, const float* k, const float* v, const elsa_shape* shp,

@@ -122,3 +122,17 @@ def test_empty_problem_is_a_noop():
     fake = ctypes.c_void_p(16)
     assert h.elsa_fwd_f32(fake, fake, fake, fake, ctypes.byref(s), ctypes.c_double(0.1), 0,
                           None, 0, None) == 0
+
+
+def test_host_entry_validates_before_touching_the_device():
+    # elsa_fwd_f32_host takes dense host arrays; a non-dense stride or a
+    # missing pointer is a ShapeError before any CUDA call
+    h = _lib.lib()
+    s = _shape(2, 3, 128, 128)
+    buf = (ctypes.c_float * 4)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    s.q_stride[2] = 68  # padded rows: not the dense layout
+    assert h.elsa_fwd_f32_host(p, p, p, p, ctypes.byref(s), 0.125, 0, None, 0, None) == 2
+    s = _shape(2, 3, 128, 128)
+    assert h.elsa_fwd_f32_host(None, p, p, p, ctypes.byref(s), 0.125, 0, None, 0, None) == 2
+    assert h.elsa_fwd_f32_host(p, p, p, p, ctypes.byref(s), float("nan"), 0, None, 0, None) == 2
