@@ -45,6 +45,32 @@
 
 #include "ptx.cuh"
 
+// Compile-time tuning knobs (defaults = the shipped configuration; the
+// variant sweep in tools/variant_sweep.sh builds and times alternatives).
+// Unrolls measured on B200 (tools/variant_sweep.sh + tools/ab_time.py):
+// deep unrolls let ptxas hoist each step's shared loads well ahead of their
+// FFMA2s, which matters with only two consumer warps per SM sub-partition.
+//   R = 16 (w8r16): GEMM1 d/4 loop x4, GEMM2 key loop x16   (16K: 49.8 -> 56.5 TFLOP/s)
+//   R = 8 (w4r8, w8r8): GEMM1 fully unrolled, GEMM2 x16     (4K: 47.0 -> 54.8)
+#ifndef ELSA_G1_UNROLL_R16
+#define ELSA_G1_UNROLL_R16 4
+#endif
+#ifndef ELSA_G1_UNROLL_R8
+#define ELSA_G1_UNROLL_R8 16
+#endif
+#ifndef ELSA_G2_UNROLL
+#define ELSA_G2_UNROLL 16  // unroll of GEMM2's key loop
+#endif
+#ifndef ELSA_SNAKE
+#define ELSA_SNAKE 1      // reverse the row-pair order on odd broadcast operands
+#endif
+#ifndef ELSA_CONSUMER_REGS
+#define ELSA_CONSUMER_REGS 224
+#endif
+#ifndef ELSA_PRODUCER_REGS
+#define ELSA_PRODUCER_REGS 40
+#endif
+
 namespace elsa {
 
 enum FwdMode : int {
@@ -154,12 +180,14 @@ struct FwdTraits {
   static constexpr int MAX_REGS = (16384 / (WARPS_PER_SMSP * 32)) / 8 * 8 > 255
                                       ? 255
                                       : (16384 / (WARPS_PER_SMSP * 32)) / 8 * 8;
-  static constexpr int PRODUCER_REGS = 40;
+  static constexpr int PRODUCER_REGS = ELSA_PRODUCER_REGS;
+  static constexpr int G1_UNROLL = R >= 16 ? ELSA_G1_UNROLL_R16 : ELSA_G1_UNROLL_R8;
+  static constexpr int G2_UNROLL = ELSA_G2_UNROLL;
   // Phase-offsetting the two warps of each SMSP (see `lagged` in the kernel)
   // measured no gain on B200 (per-warp phase trace) and costs registers, so
   // it is compiled out.
   static constexpr bool kLag = false;
-  static constexpr int CONSUMER_REGS = 224;  // after setmaxnreg.inc (R = 16 only)
+  static constexpr int CONSUMER_REGS = ELSA_CONSUMER_REGS;  // after setmaxnreg.inc (R = 16 only)
   static_assert(!kRegSplit || (W % 4 == 0), "register split needs whole consumer warpgroups");
   static_assert(!kRegSplit || PRODUCER_REGS + (W / 4) * CONSUMER_REGS <= 512,
                 "per-SMSP register budget after setmaxnreg");
@@ -357,7 +385,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
   auto gemm2_release = [&](int tt) {
     const int st = tt % T::STAGES;
     const float* vs = Vs + st * T::V_FLOATS + 4 * g;
-#pragma unroll 2
+#pragma unroll(T::G2_UNROLL)
     for (int jj = 0; jj < TK; ++jj) {
       f32x2 pr[RP];
 #pragma unroll
@@ -370,7 +398,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
         const f32x2 vb = ptx::pack2(vv, vv);
 #pragma unroll
         for (int u = 0; u < RP; ++u) {
-          const int ip = (c & 1) ? RP - 1 - u : u;
+          const int ip = (ELSA_SNAKE && (c & 1)) ? RP - 1 - u : u;
           ptx::ffma2(o2[ip][c], vb, pr[ip]);
         }
       }
@@ -401,7 +429,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
 #pragma unroll
       for (int j = 0; j < RK; ++j) s2[ip][j] = 0ull;
 
-#pragma unroll 1
+#pragma unroll(T::G1_UNROLL)
     for (int c = 0; c < T::D / 4; ++c) {
       float4 kf[RK];
 #pragma unroll
@@ -418,7 +446,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
           const f32x2 kb = ptx::pack2(kv, kv);
 #pragma unroll
           for (int u = 0; u < RP; ++u) {
-            const int ip = (j & 1) ? RP - 1 - u : u;
+            const int ip = (ELSA_SNAKE && (j & 1)) ? RP - 1 - u : u;
             ptx::ffma2(s2[ip][j], kb, q2[ip]);
           }
         }

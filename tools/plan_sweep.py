@@ -13,6 +13,8 @@ for _ in range(40):
     _w = _w @ _w.T * 1e-4
 torch.cuda.synchronize()
 shapes = [(1, 16, 1024), (8, 12, 512), (1, 1, 1024), (1, 16, 2048), (1, 16, 4096)]
+if os.environ.get("PLAN_SHAPES"):
+    shapes = [tuple(int(x) for x in s.split("x")) for s in os.environ["PLAN_SHAPES"].split(",")]
 for (b, h, n) in shapes:
     q, k, v = (torch.randn(b, h, n, 64, device="cuda") for _ in range(3))
     for splits in (1, 2, 3, 4, 6, 8, 16):
