@@ -38,6 +38,7 @@ from .attention import (  # noqa: F401
     bound_threshold,
     naive_attention,
     partial_state_fp64,
+    row_err_conditioned,
     row_rel_err,
     sampled_rows_fp64,
     vectorized_probs,

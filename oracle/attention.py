@@ -122,6 +122,23 @@ def bound_threshold(n, block_size=128, slack=DEFAULT_SLACK):
     return U32 * scan_depth(n, block_size) * slack
 
 
+def row_err_conditioned(y, Q, K, V, ref=None, scale=None):
+    """Per-row error scaled by the row's conditioning instead of |y|:
+    ||y_hat - y||_2 / ||sum_j p_j |v_j| ||_2 with p the FP64 softmax row.
+    Y is a convex combination of V rows, so this is the forward error of that
+    combination relative to the magnitudes it combines; it stays meaningful
+    when a narrow (d_v <= 2) output row cancels to ~0, where the relative
+    error of row_rel_err is unbounded for any finite-precision method (the
+    reference's own FP32 scan included). Test-only helper, FP64 throughout."""
+    y = np.asarray(y, dtype=np.float64)
+    if ref is None:
+        ref = naive_attention(Q, K, V, scale=scale)
+    _, P = naive_attention(Q, K, V, scale=scale, return_p=True)
+    mag = np.matmul(P, np.abs(np.asarray(V, dtype=np.float64)))
+    tiny = np.finfo(np.float64).tiny
+    return np.linalg.norm(y - ref, axis=-1) / np.maximum(np.linalg.norm(mag, axis=-1), tiny)
+
+
 def row_rel_err(y, ref):
     """Per-row relative L2 error against a reference (verify.py:336-338)."""
     y = np.asarray(y, dtype=np.float64)

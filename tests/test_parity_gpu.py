@@ -143,10 +143,15 @@ def test_head_dims(d, dv):
     assert y.shape == (1, 2, 200, dv)
     ref = oracle.naive_attention(Q, K, V)
     if dv <= 2:
-        # a 1-2 wide output row can sit near 0 (cancellation): gate against
-        # the reference FP32 scan's own error instead of the relative bound
-        ref32 = oracle.scan_forward_port(Q, K, V)
-        assert_relative_to_reference(y, ref, ref32, 200, f"d{d} dv{dv}")
+        # a 1-2 wide output row can cancel to ~0, where the per-row relative
+        # error is unbounded for any FP32 method (the reference scan's own
+        # p99 exceeds u*L*8 on some seeds): bound the error relative to the
+        # magnitudes the convex combination mixes instead, plus the aggregate
+        err = oracle.row_err_conditioned(y, Q, K, V, ref=ref)
+        thr = oracle.bound_threshold(200)
+        assert err.max() <= thr, f"d{d} dv{dv}: conditioned row err {err.max():.3e} > {thr:.3e}"
+        agg = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+        assert agg <= thr, f"d{d} dv{dv}: aggregate rel-L2 {agg:.3e} > {thr:.3e}"
     else:
         assert_bound(y, ref, 200, f"d{d} dv{dv}")
 
