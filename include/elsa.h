@@ -167,6 +167,12 @@ int elsa_block_scan_f32(const float* m, const float* S, const float* W,
                         float* pre_m, float* pre_S, float* pre_W,
                         void* workspace, size_t ws_bytes, void* stream);
 
+/* Device memory for callers without a CUDA allocator of their own (e.g. a
+ * numpy/ctypes binding sizing the workspace of elsa_fwd_f32_host): thin
+ * cudaMalloc / cudaFree on the current device. Never used on the hot path. */
+int elsa_device_alloc(size_t bytes, void** ptr);
+int elsa_device_free(void* ptr);
+
 /* Synchronises `stream`, returns the device error word (0 = none, else an
  * elsa_status) through *code, and clears it. */
 int elsa_get_device_error(void* stream, int* code);

@@ -35,6 +35,8 @@ EXPORTED_SYMBOLS = (
     "elsa_blockwise_f32",
     "elsa_block_scan_workspace_bytes",
     "elsa_block_scan_f32",
+    "elsa_device_alloc",
+    "elsa_device_free",
     "elsa_get_device_error",
     "elsa_ffma_peak",
     "elsa_last_launch_count",
@@ -108,6 +110,10 @@ def _declare(h):
     h.elsa_block_scan_f32.restype = c_int
     h.elsa_block_scan_f32.argtypes = [c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_vp, c_vp,
                                       c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]
+    h.elsa_device_alloc.restype = c_int
+    h.elsa_device_alloc.argtypes = [c_sz, ctypes.POINTER(c_vp)]
+    h.elsa_device_free.restype = c_int
+    h.elsa_device_free.argtypes = [c_vp]
     h.elsa_get_device_error.restype = c_int
     h.elsa_get_device_error.argtypes = [c_vp, ctypes.POINTER(c_int)]
     h.elsa_ffma_peak.restype = c_int

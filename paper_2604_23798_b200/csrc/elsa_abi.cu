@@ -961,6 +961,20 @@ int elsa_block_scan_f32(const float* m, const float* S, const float* W, int64_t 
   return ELSA_OK;
 }
 
+int elsa_device_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return ELSA_ERR_SHAPE;
+  *ptr = nullptr;
+  if (bytes == 0) return ELSA_OK;
+  const cudaError_t e = cudaMalloc(ptr, bytes);
+  return e == cudaSuccess ? ELSA_OK : cuda_fail(e, "cudaMalloc");
+}
+
+int elsa_device_free(void* ptr) {
+  if (!ptr) return ELSA_OK;
+  const cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? ELSA_OK : cuda_fail(e, "cudaFree");
+}
+
 int elsa_get_device_error(void* stream, int* code) {
   if (!code) return ELSA_ERR_SHAPE;
   DeviceCache* dc = nullptr;

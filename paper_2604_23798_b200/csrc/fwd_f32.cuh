@@ -58,8 +58,11 @@
 #ifndef ELSA_G1_UNROLL_R8
 #define ELSA_G1_UNROLL_R8 16
 #endif
-#ifndef ELSA_G2_UNROLL
-#define ELSA_G2_UNROLL 16  // unroll of GEMM2's key loop
+#ifndef ELSA_G2_UNROLL_R16
+#define ELSA_G2_UNROLL_R16 16
+#endif
+#ifndef ELSA_G2_UNROLL_R8
+#define ELSA_G2_UNROLL_R8 16
 #endif
 #ifndef ELSA_SNAKE
 #define ELSA_SNAKE 1      // reverse the row-pair order on odd broadcast operands
@@ -182,7 +185,7 @@ struct FwdTraits {
                                       : (16384 / (WARPS_PER_SMSP * 32)) / 8 * 8;
   static constexpr int PRODUCER_REGS = ELSA_PRODUCER_REGS;
   static constexpr int G1_UNROLL = R >= 16 ? ELSA_G1_UNROLL_R16 : ELSA_G1_UNROLL_R8;
-  static constexpr int G2_UNROLL = ELSA_G2_UNROLL;
+  static constexpr int G2_UNROLL = R >= 16 ? ELSA_G2_UNROLL_R16 : ELSA_G2_UNROLL_R8;
   // Phase-offsetting the two warps of each SMSP (see `lagged` in the kernel)
   // measured no gain on B200 (per-warp phase trace) and costs registers, so
   // it is compiled out.

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+for v in build/var_*.so; do
+  n=$(basename $v .so)
+  for c in w8r16 w8r8 w4r8; do
+    AB_SHAPES=1x16x4096,1x16x16384 ELSA_FWD_CFG=$c ELSA_LIB_PATH=$v timeout 150 python tools/ab_time.py ${n}_$c || echo "$v $c failed"
+  done
+done

@@ -1,7 +1,9 @@
 """Time K5 (tcgen05 FP16/BF16) against torch SDPA (flash backend) on the same
 inputs; CUDA-graph replays, L2 flushed between, events on the capture stream."""
+import os
 import sys
-import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
 import paper_2604_23798_b200 as elsa
 
 dev = torch.device("cuda", 0)
