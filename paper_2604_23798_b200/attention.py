@@ -351,7 +351,10 @@ def partial_states(query, key, value, kv_begin=0, kv_end=None, scale=None, kv_sp
         # workspace for the internal split tree, sized for the requested count
         ws_bytes = 0
         if kv_splits != 1:
-            ws_bytes = h.elsa_workspace_bytes(ctypes.byref(shp), int(kv_splits))
+            # the plan (and its workspace) is made for the key range, not n_kv
+            rng = _lib.ElsaShape.from_buffer_copy(shp)
+            rng.n_kv = max(int(kv_end) - int(kv_begin), 1)
+            ws_bytes = h.elsa_workspace_bytes(ctypes.byref(rng), int(kv_splits))
         ws = torch.empty(max(ws_bytes, 1), device=q.device, dtype=torch.uint8) if ws_bytes else None
         st = h.elsa_partial_f32(
             ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),

@@ -70,6 +70,9 @@
 #ifndef ELSA_CONSUMER_REGS
 #define ELSA_CONSUMER_REGS 224
 #endif
+#ifndef ELSA_PRODUCER_SLEEP_NS
+#define ELSA_PRODUCER_SLEEP_NS 256  // back-off between the producer's empty-slot polls
+#endif
 #ifndef ELSA_PRODUCER_REGS
 #define ELSA_PRODUCER_REGS 40
 #endif
@@ -230,7 +233,7 @@ __device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw
   const float* vg = p.v + int64_t(b) * p.vs_b + int64_t(h) * p.vs_h;
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % T::STAGES;
-    if (t >= T::STAGES) ptx::mbar_wait(&empty[s], ((t / T::STAGES) - 1) & 1);
+    if (t >= T::STAGES) ptx::mbar_wait_backoff(&empty[s], ((t / T::STAGES) - 1) & 1, ELSA_PRODUCER_SLEEP_NS);
     const int key0 = split_lo + t * T::TK;
     float* ks = Ks + s * T::K_FLOATS;
     float* vs = Vs + s * T::V_FLOATS;
@@ -318,7 +321,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
         ptx::tma_load_4d(Qraw, &tmQ, qbar, 0, q0, h, b);
         for (int t = 0; t < ntiles; ++t) {
           const int s = t % T::STAGES;
-          if (t >= T::STAGES) ptx::mbar_wait(&empty[s], ((t / T::STAGES) - 1) & 1);
+          if (t >= T::STAGES) ptx::mbar_wait_backoff(&empty[s], ((t / T::STAGES) - 1) & 1, ELSA_PRODUCER_SLEEP_NS);
           const int key0 = split_lo + t * TK;
           ptx::mbar_arrive_expect_tx(&full[s], T::KV_TX_BYTES);
           ptx::tma_load_4d(Ks + s * T::K_FLOATS, &tmK, &full[s], 0, key0, h, b);

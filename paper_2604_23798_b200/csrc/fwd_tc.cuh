@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(192, 1)
       ptx::tma_load_4d(smem + T::OFF_Q, &tmQ, qbar, 0, q0, h, b);
       for (int t = 0; t < ntiles; ++t) {
         const int s = t % T::STAGES;
-        if (t >= T::STAGES) ptx::mbar_wait(&kv_empty[s], ((t / T::STAGES) - 1) & 1);
+        if (t >= T::STAGES) ptx::mbar_wait_backoff(&kv_empty[s], ((t / T::STAGES) - 1) & 1, 64);
         ptx::mbar_arrive_expect_tx(&kv_full[s], T::K_BYTES + T::V_BYTES);
         ptx::tma_load_4d(smem + T::OFF_K + s * T::K_BYTES, &tmK, &kv_full[s], 0, t * T::TK, h, b);
         ptx::tma_load_4d(smem + T::OFF_V + s * T::V_BYTES, &tmV, &kv_full[s], 0, t * T::TK, h, b);

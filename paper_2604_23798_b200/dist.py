@@ -69,8 +69,11 @@ def shard_kv(k, v, rank, world, chunks=DEFAULT_CHUNKS):
 
 
 def _gpu_partial(q, k, v, kv_begin, kv_end):
+    # auto splits: the planner caps the per-CTA key chain (accuracy at long
+    # chunks); the plan depends only on the chunk's shape, so every world size
+    # computes each global chunk identically
     from .attention import partial_states
-    return partial_states(q, k, v, kv_begin, kv_end, kv_splits=1)
+    return partial_states(q, k, v, kv_begin, kv_end, kv_splits=0)
 
 
 def _gpu_merge(m, S, W):
