@@ -33,6 +33,7 @@ using namespace elsa;
 namespace {
 
 constexpr int kMaxDevices = 64;
+constexpr int kAttrSlots = 16;
 constexpr int kMaxSplits = kMergeMaxParts;
 constexpr double kLog2e = 1.4426950408889634074;
 
@@ -62,7 +63,7 @@ struct DeviceCache {
   bool ready = false;
   int sms = 0;
   int* err = nullptr;
-  bool attr[8] = {};
+  bool attr[kAttrSlots] = {};  // forward configs x TMA flag, then the tc kernels
 };
 DeviceCache g_dev[kMaxDevices];
 std::mutex g_mu;
@@ -807,20 +808,40 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
   if (c < 1e-30) c = 1e-30;
   p.c = float(c);
   p.neg = scale < 0 ? 1 : 0;
-  p.qtiles = int(ceil_div(shp->n_q, TcTraits::TQ));
   p.err = dc->err;
-  auto kern = bf16 ? fwd_tc_kernel<true> : fwd_tc_kernel<false>;
-  const int slot = 6 + (bf16 ? 1 : 0);
-  if (!dc->attr[slot]) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               int(TcTraits::SMEM_BYTES));
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc)");
-    dc->attr[slot] = true;
-  }
-  const int64_t gx = int64_t(p.qtiles) * shp->B * shp->H;
-  if (gx >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
-  kern<<<unsigned(gx), TcTraits::THREADS, TcTraits::SMEM_BYTES,
-         static_cast<cudaStream_t>(stream)>>>(p, maps[0], maps[1], maps[2]);
+  // two query tiles (two softmax warpgroups) per CTA when that still fills the
+  // GPU a few times over; ELSA_TC_GROUPS forces 1 or 2
+  static const int forced_groups = [] {
+    const char* e = std::getenv("ELSA_TC_GROUPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int64_t BH = shp->B * shp->H;
+  int groups = ceil_div(shp->n_q, 256) * BH >= 2 * int64_t(dc->sms) ? 2 : 1;
+  if (forced_groups == 1 || forced_groups == 2) groups = forced_groups;
+  auto launch = [&](auto traits, auto kern, int slot) -> int {
+    using TT = decltype(traits);
+    p.qtiles = int(ceil_div(shp->n_q, TT::ROWS));
+    if (!dc->attr[slot]) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(TT::SMEM_BYTES));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc)");
+      dc->attr[slot] = true;
+    }
+    const int64_t gx = int64_t(p.qtiles) * BH;
+    if (gx >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
+    kern<<<unsigned(gx), TT::THREADS, TT::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
+        p, maps[0], maps[1], maps[2]);
+    return ELSA_OK;
+  };
+  const int base = kAttrSlots - 4;  // the last four slots
+  int st;
+  if (groups == 2)
+    st = bf16 ? launch(TcTraits<2>{}, fwd_tc_kernel<true, 2>, base + 3)
+              : launch(TcTraits<2>{}, fwd_tc_kernel<false, 2>, base + 2);
+  else
+    st = bf16 ? launch(TcTraits<1>{}, fwd_tc_kernel<true, 1>, base + 1)
+              : launch(TcTraits<1>{}, fwd_tc_kernel<false, 1>, base);
+  if (st) return st;
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "tc launch");
   ++t_last_launches;
   return ELSA_OK;

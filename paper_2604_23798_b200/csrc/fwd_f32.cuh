@@ -197,6 +197,11 @@ struct FwdTraits {
   static_assert(!kRegSplit || (W % 4 == 0), "register split needs whole consumer warpgroups");
   static_assert(!kRegSplit || PRODUCER_REGS + (W / 4) * CONSUMER_REGS <= 512,
                 "per-SMSP register budget after setmaxnreg");
+  // setmaxnreg only redistributes the launch allocation (MAX_REGS per warp):
+  // the consumers' growth must not exceed what the producer warp releases,
+  // or the .inc blocks forever (240/32 hung on B200)
+  static_assert(!kRegSplit || (W / 4) * (CONSUMER_REGS - MAX_REGS) <= MAX_REGS - PRODUCER_REGS,
+                "setmaxnreg growth exceeds the registers the producers release");
   static constexpr size_t BAR_OFFSET =
       size_t(QT_FLOATS + STAGES * (K_FLOATS + V_FLOATS) + P_FLOATS) * 4;
   static constexpr size_t SMEM_BYTES = BAR_OFFSET + (2 * STAGES + 1) * 8;

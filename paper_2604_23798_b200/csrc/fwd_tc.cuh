@@ -8,12 +8,28 @@
 //   m_t, P_t = 2^(s c - m_t) one query row per thread (tcgen05.ld 32x32b)
 //   O_t = P_t V_t            tcgen05.mma  128x64x128  -> TMEM (double buffer)
 //   W <- (W + O_{t-1}) 2^(m_{t-1} - m_t)   FP32 registers (the ⊕ of monoid.py:160-200)
-// The softmax of tile t overlaps the tensor core computing O_{t-1} and S_{t+1}.
 //
-// Warp roles (192 threads, 1 CTA / SM): warps 0-3 softmax + epilogue (warp w
-// owns TMEM lanes 32w..32w+31 = query rows), warp 4 TMA producer (Q once,
-// K/V through a 3-stage ring, 128B-swizzled 16-bit tiles), warp 5 TMEM
-// allocator + single-thread MMA issuer.
+// A CTA owns GROUPS (1 or 2) query tiles of 128 rows, one softmax warpgroup
+// each (warp w of group g owns TMEM lanes 32(w%4).. = query rows), so two
+// softmax streams share every SM sub-partition and the single MMA thread
+// ping-pongs between them: while group 0 exponentiates S_0(t), the tensor
+// core computes S_1(t) / P_1 V, and vice versa. Per group TMEM holds S (128
+// columns, single buffer: S(t+1) is issued only after the group released
+// S(t)) and the running W = O (64 columns) that P V accumulates into. P goes
+// through a 128B-swizzled smem tile per group (single buffer: written after
+// P(t-1) V completed).
+//
+// The (m, S, W) combine with a deferred anchor: a row's anchor m moves only
+// when the tile maximum exceeds it by more than kRescaleLog2 (log2 units);
+// then S and the TMEM W of that row are multiplied by 2^(m_old - m_new)
+// (tcgen05.ld / st by the owning warp, skipped warp-wide when no row of the
+// warp moved). Between moves every P = 2^(s c - m) <= 2^kRescaleLog2, exact in
+// the 16-bit formats' range; the result is the same monoid product, only the
+// anchor at which each partial sum is represented differs.
+//
+// Warp roles (GROUPS*128 + 64 threads, 1 CTA / SM): softmax warpgroups, then
+// a TMA producer warp (Q once, K/V through a 3-stage ring, 128B-swizzled
+// 16-bit tiles) and the TMEM allocator + single-thread MMA issuer warp.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -31,37 +47,53 @@ struct TcParams {
   int64_t ys_b, ys_h, ys_r;  // element strides of y
   float c;                   // |scale| * log2(e)
   int neg;                   // scale < 0 (sign applied to the scores)
-  int qtiles;
+  int qtiles;                // CTAs per (b, h): ceil(n_q / (GROUPS * 128))
   int* err;
 };
 
+// anchor hysteresis of the deferred rescale (log2 units): P <= 2^8
+constexpr float kRescaleLog2 = 8.f;
+
+template <int GROUPS>
 struct TcTraits {
   static constexpr int TQ = 128, TK = 128, D = 64, STAGES = 3;
+  static constexpr int ROWS = GROUPS * TQ;                   // query rows per CTA
   static constexpr int ROW_BYTES = D * 2;                    // 128 B per 16-bit row
-  static constexpr int Q_BYTES = TQ * ROW_BYTES;             // 16 KB
+  static constexpr int Q_BYTES = TQ * ROW_BYTES;             // 16 KB per group
   static constexpr int K_BYTES = TK * ROW_BYTES;             // 16 KB
   static constexpr int V_BYTES = TK * ROW_BYTES;             // 16 KB
-  static constexpr int P_BYTES = TQ * TK * 2;                // 32 KB (two 64-key chunks)
+  static constexpr int P_BYTES = TQ * TK * 2;                // 32 KB per group (two 64-key chunks)
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_K = OFF_Q + GROUPS * Q_BYTES;
   static constexpr int OFF_V = OFF_K + STAGES * K_BYTES;
   static constexpr int OFF_P = OFF_V + STAGES * V_BYTES;
-  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-  // barriers: qbar, kv_full[3], kv_empty[3], s_full[2], p_full[2], o_full[2], + tmem base word
-  static constexpr int NBAR = 1 + 2 * STAGES + 6;
+  static constexpr int OFF_BAR = OFF_P + GROUPS * P_BYTES;
+  // barriers: qbar, kv_full[3], kv_empty[3], s_full[G], p_full[G], o_full[G], + tmem base word
+  static constexpr int NBAR = 1 + 2 * STAGES + 3 * GROUPS;
   static constexpr size_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16 + 1024;  // + 1024 alignment slack
-  static constexpr int THREADS = 192;
-  static constexpr uint32_t TMEM_COLS = 512;
-  static constexpr uint32_t S_COL = 0;    // S buffers at columns 0 and 128
-  static constexpr uint32_t O_COL = 256;  // O buffers at columns 256 and 320
+  static constexpr int SOFTMAX_WARPS = 4 * GROUPS;
+  static constexpr int TMA_WARP = SOFTMAX_WARPS, MMA_WARP = SOFTMAX_WARPS + 1;
+  // GROUPS = 2: a whole third warpgroup (TMA, MMA, two idle warps) so setmaxnreg
+  // can hand its registers to the softmax warpgroups; 12 warps launch at 168
+  // and setmaxnreg only redistributes that allocation (per SM sub-partition
+  // 3 x 168 = 504): 168 - 40 = 128 freed = 2 x (232 - 168) taken. Asking for
+  // more than is freed blocks the .inc forever.
+  static constexpr bool kRegSplit = GROUPS == 2;
+  static constexpr int THREADS = kRegSplit ? (SOFTMAX_WARPS + 4) * 32 : (SOFTMAX_WARPS + 2) * 32;
+  static constexpr int SOFTMAX_REGS = 232, OTHER_REGS = 40;
+  static_assert(!kRegSplit || 2 * (SOFTMAX_REGS - 168) <= 168 - OTHER_REGS, "setmaxnreg budget");
+  static constexpr uint32_t TMEM_COLS = GROUPS == 1 ? 256 : 512;
+  static constexpr uint32_t S_COL = 0;    // group g: S at 128 g
+  static constexpr uint32_t O_COL = 256;  // group g: W (P V accumulator) at 256 + 64 g
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
-template <bool kBF16>
-__global__ void __launch_bounds__(192, 1)
+template <bool kBF16, int GROUPS>
+__global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
                   const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV) {
-  using T = TcTraits;
+  using T = TcTraits<GROUPS>;
   extern __shared__ unsigned char smem_dyn[];
   // 1024-byte alignment for the 128B-swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -71,9 +103,9 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + T::STAGES;
   uint64_t* s_full = kv_empty + T::STAGES;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* o_full = p_full + 2;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  uint64_t* p_full = s_full + GROUPS;
+  uint64_t* o_full = p_full + GROUPS;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(o_full + GROUPS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -81,7 +113,7 @@ __global__ void __launch_bounds__(192, 1)
   const int bh = blockIdx.x / p.qtiles;
   const int b = bh / p.H;
   const int h = bh - b * p.H;
-  const int q0 = qtile * T::TQ;
+  const int q0 = qtile * T::ROWS;
   const int ntiles = (p.n_kv + T::TK - 1) / T::TK;
 
   if (threadIdx.x == 0) {
@@ -90,14 +122,14 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mbar_init(&kv_full[s], 1);
       ptx::mbar_init(&kv_empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&p_full[i], 128);
-      ptx::mbar_init(&o_full[i], 1);
+    for (int g = 0; g < GROUPS; ++g) {
+      ptx::mbar_init(&s_full[g], 1);
+      ptx::mbar_init(&p_full[g], 128);
+      ptx::mbar_init(&o_full[g], 1);
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 5) tc::tmem_alloc(tmem_base_slot, T::TMEM_COLS);
+  if (warp == T::MMA_WARP) tc::tmem_alloc(tmem_base_slot, T::TMEM_COLS);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -107,14 +139,20 @@ __global__ void __launch_bounds__(192, 1)
   constexpr uint32_t kIdescS = tc::instr_desc_f16(kFmt, false, false, 128, 128);
   constexpr uint32_t kIdescO = tc::instr_desc_f16(kFmt, false, true, 128, 64);
 
-  if (warp == 4) {
+  // setmaxnreg inside each role's branch so the softmax code is dominated by
+  // the .inc (ptxas then allocates up to SOFTMAX_REGS there)
+  if (warp >= T::SOFTMAX_WARPS) {
+    if constexpr (T::kRegSplit) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(T::OTHER_REGS));
+  }
+  if (warp == T::TMA_WARP) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       ptx::prefetch_tmap(&tmQ);
       ptx::prefetch_tmap(&tmK);
       ptx::prefetch_tmap(&tmV);
-      ptx::mbar_arrive_expect_tx(qbar, T::Q_BYTES);
-      ptx::tma_load_4d(smem + T::OFF_Q, &tmQ, qbar, 0, q0, h, b);
+      ptx::mbar_arrive_expect_tx(qbar, GROUPS * T::Q_BYTES);
+      for (int g = 0; g < GROUPS; ++g)  // rows past n_q are zero-filled by TMA
+        ptx::tma_load_4d(smem + T::OFF_Q + g * T::Q_BYTES, &tmQ, qbar, 0, q0 + g * T::TQ, h, b);
       for (int t = 0; t < ntiles; ++t) {
         const int s = t % T::STAGES;
         if (t >= T::STAGES) ptx::mbar_wait_backoff(&kv_empty[s], ((t / T::STAGES) - 1) & 1, 64);
@@ -123,31 +161,27 @@ __global__ void __launch_bounds__(192, 1)
         ptx::tma_load_4d(smem + T::OFF_V + s * T::V_BYTES, &tmV, &kv_full[s], 0, t * T::TK, h, b);
       }
     }
-  } else if (warp == 5) {
-    // ---------------- MMA issuer ----------------
+  } else if (warp == T::MMA_WARP) {
+    // ---------------- MMA issuer (one thread) ----------------
     if (lane == 0) {
-      const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q);
-      auto issue_s = [&](int t) {
+      auto issue_s = [&](int g, int t) {  // S_g(t) = Q_g K_t^T
         const int s = t % T::STAGES;
-        ptx::mbar_wait(&kv_full[s], (t / T::STAGES) & 1);
-        tc::fence_after_sync();
+        const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q + g * T::Q_BYTES);
         const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K + s * T::K_BYTES);
-        const uint32_t d = tmem + T::S_COL + (t & 1) * 128;
+        const uint32_t d = tmem + T::S_COL + g * 128;
 #pragma unroll
         for (int kk = 0; kk < T::D / 16; ++kk) {  // K-steps of 16 elements = 32 B
           const uint64_t a = tc::smem_desc_sw128(q_addr + kk * 32, 16, 1024);
           const uint64_t bd = tc::smem_desc_sw128(k_addr + kk * 32, 16, 1024);
           tc::mma_f16_ss(d, a, bd, kIdescS, kk > 0);
         }
-        tc::commit(&s_full[t & 1]);
+        tc::commit(&s_full[g]);
       };
-      auto issue_o = [&](int t) {
+      auto issue_o = [&](int g, int t) {  // W_g (+)= P_g(t) V_t
         const int s = t % T::STAGES;
-        ptx::mbar_wait(&p_full[t & 1], (t >> 1) & 1);
-        tc::fence_after_sync();
-        const uint32_t p_addr = ptx::smem_u32(smem + T::OFF_P + (t & 1) * T::P_BYTES);
+        const uint32_t p_addr = ptx::smem_u32(smem + T::OFF_P + g * T::P_BYTES);
         const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V + s * T::V_BYTES);
-        const uint32_t d = tmem + T::O_COL + (t & 1) * 64;
+        const uint32_t d = tmem + T::O_COL + g * 64;
 #pragma unroll
         for (int kk = 0; kk < T::TK / 16; ++kk) {
           // P: K-major, two 64-key chunks of 128 rows x 128 B
@@ -155,67 +189,110 @@ __global__ void __launch_bounds__(192, 1)
           const uint64_t a = tc::smem_desc_sw128(pa, 16, 1024);
           // V: MN-major (rows = keys, 128 B each); 16 keys per step = 2 swizzle atoms
           const uint64_t bd = tc::smem_desc_sw128(v_addr + kk * 2048, 16, 1024);
-          tc::mma_f16_ss(d, a, bd, kIdescO, kk > 0);
+          tc::mma_f16_ss(d, a, bd, kIdescO, (t > 0 || kk > 0) ? 1u : 0u);
         }
-        tc::commit(&o_full[t & 1]);
-        tc::commit(&kv_empty[s]);
+        tc::commit(&o_full[g]);
       };
       ptx::mbar_wait(qbar, 0);
-      tc::fence_after_sync();
-      if (ntiles > 0) issue_s(0);
-      for (int t = 1; t <= ntiles; ++t) {
-        if (t < ntiles) issue_s(t);  // S buffer t&1 was released by p_full(t-2), awaited below
-        issue_o(t - 1);
+      if (ntiles > 0) {
+        ptx::mbar_wait(&kv_full[0], 0);
+        tc::fence_after_sync();
+        for (int g = 0; g < GROUPS; ++g) issue_s(g, 0);
+      }
+      for (int t = 0; t < ntiles; ++t) {
+        for (int g = 0; g < GROUPS; ++g) {
+          // group g released S_g(t), wrote P_g(t) and rescaled its W if needed
+          ptx::mbar_wait(&p_full[g], t & 1);
+          tc::fence_after_sync();
+          issue_o(g, t);
+          if (g == GROUPS - 1) tc::commit(&kv_empty[t % T::STAGES]);  // K_t, V_t consumed
+          if (t + 1 < ntiles) {
+            if (g == 0) {
+              ptx::mbar_wait(&kv_full[(t + 1) % T::STAGES], ((t + 1) / T::STAGES) & 1);
+              tc::fence_after_sync();
+            }
+            issue_s(g, t + 1);
+          }
+        }
       }
     }
-  } else {
-    // ---------------- softmax + combine + epilogue (128 threads, one row each) ----------------
-    const int row = warp * 32 + lane;
-    const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  } else if (warp < T::SOFTMAX_WARPS) {
+    // ------------- softmax + combine + epilogue (one warpgroup per query tile) -------------
+    if constexpr (T::kRegSplit) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(T::SOFTMAX_REGS));
+    const int g = warp >> 2;
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+    const uint32_t s_tm = tmem + lane_base + T::S_COL + g * 128;
+    const uint32_t o_tm = tmem + lane_base + T::O_COL + g * 64;
     const float c2 = p.c;
-    const float sgn = p.neg ? -1.f : 1.f;
-    float m_run = -CUDART_INF_F;  // log2-domain anchor
+    const float cs = p.neg ? -c2 : c2;  // exponent = s_raw * cs - m
+    float m_run = -CUDART_INF_F;        // log2-domain anchor
     float l_run = 0.f;
-    float w[64];
-#pragma unroll
-    for (int i = 0; i < 64; ++i) w[i] = 0.f;
-    unsigned char* pbase = smem + T::OFF_P;
+    const uint32_t prow_s = ptx::smem_u32(smem + T::OFF_P + g * T::P_BYTES);
 
     for (int t = 0; t < ntiles; ++t) {
-      // ---- S_t row -> registers ----
-      ptx::mbar_wait(&s_full[t & 1], (t >> 1) & 1);
+      ptx::mbar_wait(&s_full[g], t & 1);
       tc::fence_after_sync();
       float s[128];
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(tmem + lane_base + T::S_COL + (t & 1) * 128 + ch * 32, r);
-        tc::tmem_wait_ld();
+        tc::tmem_ld_32x32b_x32(s_tm + ch * 32, r);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[ch * 32 + i] = __uint_as_float(r[i]) * sgn;
+        for (int i = 0; i < 32; ++i) s[ch * 32 + i] = __uint_as_float(r[i]);
       }
-      // ---- mask, tile max, anchors ----
+      tc::tmem_wait_ld();
       const int kv_hi = p.n_kv - t * T::TK;  // valid keys in this tile
-      float mx = -CUDART_INF_F;
+      if (kv_hi < T::TK) {                   // tail tile (warp-uniform): mask past n_kv
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        if (i >= kv_hi) s[i] = -CUDART_INF_F;
-        mx = fmaxf(mx, s[i]);
+        for (int i = 0; i < 128; ++i)
+          if (i >= kv_hi) s[i] = p.neg ? CUDART_INF_F : -CUDART_INF_F;
       }
-      const float m_new = fmaxf(m_run, mx * c2);
-      const float corr = ptx::ex2(m_run - m_new);
+      // row max of the signed scores, in log2 units (warp-uniform sign branch)
+      float m_tile;
+      if (!p.neg) {
+        float mx = s[0];
+#pragma unroll
+        for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+        m_tile = mx * cs;
+      } else {
+        float mn = s[0];
+#pragma unroll
+        for (int i = 1; i < 128; ++i) mn = fminf(mn, s[i]);
+        m_tile = mn * cs;
+      }
+      // deferred anchor: move only when the tile max exceeds it by > kRescaleLog2
+      const bool move = m_tile > m_run + kRescaleLog2;
+      const float m_new = move ? m_tile : m_run;
+      const float corr = move ? ptx::ex2(m_run - m_new) : 1.f;  // 0 on the first move
       m_run = m_new;
-      // ---- P_t = 2^(s c - m) (FP32), row sum, 16-bit P into the swizzled smem tile ----
-      float psum = 0.f;
-      unsigned char* prow = pbase + (t & 1) * T::P_BYTES;
+      // P_g(t-1) V done: the P tile is free and W_g holds tiles < t
+      if (t > 0) {
+        ptx::mbar_wait(&o_full[g], (t - 1) & 1);
+        tc::fence_after_sync();
+        if (__any_sync(0xffffffffu, move)) {  // rescale this warp's W rows in TMEM
+#pragma unroll
+          for (int ch = 0; ch < 2; ++ch) {
+            uint32_t r[32];
+            tc::tmem_ld_32x32b_x32(o_tm + ch * 32, r);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+            tc::tmem_st_32x32b_x32(o_tm + ch * 32, r);
+          }
+          tc::tmem_wait_st();
+        }
+      }
+      // P_t = 2^(s c - m) (FP32), row sum, 16-bit P into the swizzled tile
+      const float neg_m = -m_new;
+      float ps0 = 0.f, ps1 = 0.f;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {  // 16-byte units of 8 keys
         float pv[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          pv[e] = ptx::ex2(fmaf(s[u * 8 + e], c2, -m_new));
-          psum += pv[e];
-        }
+        for (int e = 0; e < 8; ++e) pv[e] = ptx::ex2(fmaf(s[u * 8 + e], cs, neg_m));
+        ps0 += (pv[0] + pv[1]) + (pv[2] + pv[3]);
+        ps1 += (pv[4] + pv[5]) + (pv[6] + pv[7]);
         uint4 pk;
         if constexpr (kBF16) {
           pk.x = tc::pack_bf16x2(pv[0], pv[1]);
@@ -228,48 +305,34 @@ __global__ void __launch_bounds__(192, 1)
           pk.z = tc::pack_f16x2(pv[4], pv[5]);
           pk.w = tc::pack_f16x2(pv[6], pv[7]);
         }
-        const int chunk = u >> 3;  // 64-key chunk
+        const int chunk = u >> 3;              // 64-key chunk
         const int unit = (u & 7) ^ (row & 7);  // 128B swizzle: 16-B unit XOR row phase
-        *reinterpret_cast<uint4*>(prow + chunk * (T::TQ * 128) + row * 128 + unit * 16) = pk;
+        ptx::sts128(prow_s + chunk * (T::TQ * 128) + row * 128 + unit * 16, pk);
       }
-      l_run = fmaf(l_run, corr, psum);
-      // ---- fold O_{t-1} (relative to m_{t-1}) and rescale to m_t ----
-      if (t > 0) {
-        ptx::mbar_wait(&o_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
-        tc::fence_after_sync();
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          uint32_t r[32];
-          tc::tmem_ld_32x32b_x32(tmem + lane_base + T::O_COL + ((t - 1) & 1) * 64 + ch * 32, r);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) w[ch * 32 + i] = (w[ch * 32 + i] + __uint_as_float(r[i])) * corr;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) w[i] *= corr;
-      }
-      // P_t visible to the tensor core (async proxy); S_t / O_{t-1} TMEM reads done
+      l_run = fmaf(l_run, corr, ps0 + ps1);
+      // P_t visible to the tensor core (async proxy); S_t reads and W stores done
       ptx::fence_proxy_async_smem();
       tc::fence_before_sync();
-      ptx::mbar_arrive(&p_full[t & 1]);
+      ptx::mbar_arrive(&p_full[g]);
     }
-    // ---- last O ----
+    // ---- epilogue: Y = W / S (engine.py:375-382) in the input's 16-bit format ----
+    float w[64];
     if (ntiles > 0) {
-      const int t = ntiles - 1;
-      ptx::mbar_wait(&o_full[t & 1], (t >> 1) & 1);
+      ptx::mbar_wait(&o_full[g], (ntiles - 1) & 1);
       tc::fence_after_sync();
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
         uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(tmem + lane_base + T::O_COL + (t & 1) * 64 + ch * 32, r);
+        tc::tmem_ld_32x32b_x32(o_tm + ch * 32, r);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) w[ch * 32 + i] += __uint_as_float(r[i]);
+        for (int i = 0; i < 32; ++i) w[ch * 32 + i] = __uint_as_float(r[i]);
       }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) w[i] = 0.f;
     }
-    // ---- epilogue: Y = W / S (engine.py:375-382) in the input's 16-bit format ----
-    const int qrow = q0 + row;
+    const int qrow = q0 + g * T::TQ + row;
     if (qrow < p.n_q) {
       if (!(l_run > 0.f) || !isfinite(l_run)) atomicCAS(p.err, 0, 3);
       const float inv = 1.f / l_run;
@@ -297,7 +360,7 @@ __global__ void __launch_bounds__(192, 1)
 
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == T::MMA_WARP) {
     tc::fence_after_sync();
     tc::tmem_dealloc(tmem, T::TMEM_COLS);
   }

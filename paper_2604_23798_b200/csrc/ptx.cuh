@@ -85,6 +85,14 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 16-byte shared store by 32-bit shared address (keeps the store STS when the
+// generic pointer's address space is not provable)
+__device__ __forceinline__ void sts128(uint32_t saddr, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
 __device__ __forceinline__ float4 lds128(const float* p) {
   return *reinterpret_cast<const float4*>(p);
 }
