@@ -816,7 +816,7 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
     return e ? std::atoi(e) : 0;
   }();
   const int64_t BH = shp->B * shp->H;
-  int groups = ceil_div(shp->n_q, 256) * BH >= 2 * int64_t(dc->sms) ? 2 : 1;
+  int groups = ceil_div(shp->n_q, 256) * BH >= int64_t(dc->sms) ? 2 : 1;
   if (forced_groups == 1 || forced_groups == 2) groups = forced_groups;
   auto launch = [&](auto traits, auto kern, int slot) -> int {
     using TT = decltype(traits);

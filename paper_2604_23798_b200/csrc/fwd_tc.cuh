@@ -14,8 +14,9 @@
 // softmax streams share every SM sub-partition and the single MMA thread
 // ping-pongs between them: while group 0 exponentiates S_0(t), the tensor
 // core computes S_1(t) / P_1 V, and vice versa. Per group TMEM holds S (128
-// columns, single buffer: S(t+1) is issued only after the group released
-// S(t)) and the running W = O (64 columns) that P V accumulates into. P goes
+// columns, single buffer: S(t+1) is issued as soon as the group has loaded
+// S(t) into registers, so it overlaps the group's own exponentials) and the
+// running W = O (64 columns) that P V accumulates into. P goes
 // through a 128B-swizzled smem tile per group (single buffer: written after
 // P(t-1) V completed).
 //
@@ -68,8 +69,9 @@ struct TcTraits {
   static constexpr int OFF_V = OFF_K + STAGES * K_BYTES;
   static constexpr int OFF_P = OFF_V + STAGES * V_BYTES;
   static constexpr int OFF_BAR = OFF_P + GROUPS * P_BYTES;
-  // barriers: qbar, kv_full[3], kv_empty[3], s_full[G], p_full[G], o_full[G], + tmem base word
-  static constexpr int NBAR = 1 + 2 * STAGES + 3 * GROUPS;
+  // barriers: qbar, kv_full[3], kv_empty[3], s_full[G], s_free[G], p_full[G], o_full[G],
+  // + tmem base word
+  static constexpr int NBAR = 1 + 2 * STAGES + 4 * GROUPS;
   static constexpr size_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16 + 1024;  // + 1024 alignment slack
   static constexpr int SOFTMAX_WARPS = 4 * GROUPS;
   static constexpr int TMA_WARP = SOFTMAX_WARPS, MMA_WARP = SOFTMAX_WARPS + 1;
@@ -103,7 +105,8 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + T::STAGES;
   uint64_t* s_full = kv_empty + T::STAGES;
-  uint64_t* p_full = s_full + GROUPS;
+  uint64_t* s_free = s_full + GROUPS;
+  uint64_t* p_full = s_free + GROUPS;
   uint64_t* o_full = p_full + GROUPS;
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(o_full + GROUPS);
 
@@ -124,6 +127,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     }
     for (int g = 0; g < GROUPS; ++g) {
       ptx::mbar_init(&s_full[g], 1);
+      ptx::mbar_init(&s_free[g], 128);
       ptx::mbar_init(&p_full[g], 128);
       ptx::mbar_init(&o_full[g], 1);
     }
@@ -193,25 +197,37 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
         }
         tc::commit(&o_full[g]);
       };
+      // Event loop over both groups: S_g(t+1) is issued as soon as group g
+      // has pulled S_g(t) into registers (s_free) — it overlaps the group's own
+      // exponentials — and P_g(t) V_t as soon as P_g(t) is written (p_full).
+      // Each barrier is only ever tested for its next phase, which cannot
+      // have been overtaken (every phase needs an MMA issued here first).
       ptx::mbar_wait(qbar, 0);
-      if (ntiles > 0) {
-        ptx::mbar_wait(&kv_full[0], 0);
-        tc::fence_after_sync();
-        for (int g = 0; g < GROUPS; ++g) issue_s(g, 0);
-      }
-      for (int t = 0; t < ntiles; ++t) {
+      int ns[GROUPS], npv[GROUPS];  // next S tile / next P V tile per group
+      for (int g = 0; g < GROUPS; ++g) ns[g] = npv[g] = 0;
+      int kv_released = 0;  // tiles whose K/V stage was handed back
+      while (kv_released < ntiles) {
+#pragma unroll
         for (int g = 0; g < GROUPS; ++g) {
-          // group g released S_g(t), wrote P_g(t) and rescaled its W if needed
-          ptx::mbar_wait(&p_full[g], t & 1);
-          tc::fence_after_sync();
-          issue_o(g, t);
-          if (g == GROUPS - 1) tc::commit(&kv_empty[t % T::STAGES]);  // K_t, V_t consumed
-          if (t + 1 < ntiles) {
-            if (g == 0) {
-              ptx::mbar_wait(&kv_full[(t + 1) % T::STAGES], ((t + 1) / T::STAGES) & 1);
-              tc::fence_after_sync();
+          const int t = ns[g];
+          if (t < ntiles && (t == 0 || ptx::mbar_try_wait(&s_free[g], (t - 1) & 1)) &&
+              ptx::mbar_try_wait(&kv_full[t % T::STAGES], (t / T::STAGES) & 1)) {
+            tc::fence_after_sync();
+            issue_s(g, t);
+            ns[g] = t + 1;
+          }
+          const int u = npv[g];
+          if (u < ns[g] && ptx::mbar_try_wait(&p_full[g], u & 1)) {
+            tc::fence_after_sync();
+            issue_o(g, u);
+            npv[g] = u + 1;
+            int done = npv[0];
+#pragma unroll
+            for (int gg = 1; gg < GROUPS; ++gg) done = npv[gg] < done ? npv[gg] : done;
+            if (done > kv_released) {  // P V of tile kv_released issued for every group
+              tc::commit(&kv_empty[kv_released % T::STAGES]);
+              ++kv_released;
             }
-            issue_s(g, t + 1);
           }
         }
       }
@@ -242,6 +258,9 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
         for (int i = 0; i < 32; ++i) s[ch * 32 + i] = __uint_as_float(r[i]);
       }
       tc::tmem_wait_ld();
+      // S_g(t) is in registers: the tensor core may overwrite it with S_g(t+1)
+      tc::fence_before_sync();
+      ptx::mbar_arrive(&s_free[g]);
       const int kv_hi = p.n_kv - t * T::TK;  // valid keys in this tile
       if (kv_hi < T::TK) {                   // tail tile (warp-uniform): mask past n_kv
 #pragma unroll
