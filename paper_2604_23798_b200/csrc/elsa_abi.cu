@@ -1066,6 +1066,22 @@ int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n
   return ELSA_OK;
 }
 
+// Development aid (ELSA_TC_TRACE builds only; not part of include/elsa.h):
+// copies K5's per-tile clock stamps (16 slots x kTcTraceTiles x 8) to `out`.
+int elsa_dev_read_tc_trace(unsigned long long* out, size_t n) {
+#ifdef ELSA_TC_TRACE
+  const size_t total = 16 * kTcTraceTiles * 8;
+  if (n > total) n = total;
+  return cudaMemcpyFromSymbol(out, g_tc_trace, n * sizeof(unsigned long long)) == cudaSuccess
+             ? ELSA_OK
+             : ELSA_ERR_CUDA;
+#else
+  (void)out;
+  (void)n;
+  return ELSA_ERR_SHAPE;
+#endif
+}
+
 // Development aid (ELSA_TRACE builds only; not part of include/elsa.h):
 // copies the phase-timestamp buffer to host memory `out` (n entries).
 int elsa_dev_read_trace(unsigned long long* out, size_t n) {

@@ -52,6 +52,26 @@ struct TcParams {
   int* err;
 };
 
+// ELSA_TC_TRACE builds: CTA 0 records SM clock stamps per tile for the first
+// kTcTraceTiles tiles: softmax warps (lane 0) at 6 points, the MMA warp at
+// its S / PV issues (diagnostic only; tools/trace_tc.py).
+constexpr int kTcTraceTiles = 64;
+#ifdef ELSA_TC_TRACE
+__device__ unsigned long long g_tc_trace[16 * kTcTraceTiles * 8];
+#define TC_MARK(slot, t, pt)                                                            \
+  do {                                                                                \
+    if (blockIdx.x == 0 && (t) < kTcTraceTiles) {                                      \
+      unsigned long long c_;                                                           \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_));                               \
+      g_tc_trace[((slot) * kTcTraceTiles + (t)) * 8 + (pt)] = c_;                      \
+    }                                                                                 \
+  } while (0)
+#else
+#define TC_MARK(slot, t, pt) \
+  do {                       \
+  } while (0)
+#endif
+
 // anchor hysteresis of the deferred rescale (log2 units): P <= 2^8
 constexpr float kRescaleLog2 = 8.f;
 
@@ -166,68 +186,82 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       }
     }
   } else if (warp == T::MMA_WARP) {
-    // ---------------- MMA issuer (one thread) ----------------
-    if (lane == 0) {
-      auto issue_s = [&](int g, int t) {  // S_g(t) = Q_g K_t^T
-        const int s = t % T::STAGES;
-        const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q + g * T::Q_BYTES);
-        const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K + s * T::K_BYTES);
-        const uint32_t d = tmem + T::S_COL + g * 128;
+    // ---------------- MMA issuer ----------------
+    // The whole warp runs the (warp-uniform) schedule so the descriptors stay
+    // in uniform registers; one elected lane issues each tcgen05.mma / commit.
+    // (A lane-0-only loop paid R2UR round trips per descriptor and measured
+    // ~1300 clocks from a group's barrier to the matching issue.)
+    const bool leader = tc::elect_one();
+    auto issue_s = [&](int g, int t) {  // S_g(t) = Q_g K_t^T
+      const int s = t % T::STAGES;
+      const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q + g * T::Q_BYTES);
+      const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K + s * T::K_BYTES);
+      const uint32_t d = tmem + T::S_COL + g * 128;
 #pragma unroll
-        for (int kk = 0; kk < T::D / 16; ++kk) {  // K-steps of 16 elements = 32 B
-          const uint64_t a = tc::smem_desc_sw128(q_addr + kk * 32, 16, 1024);
-          const uint64_t bd = tc::smem_desc_sw128(k_addr + kk * 32, 16, 1024);
-          tc::mma_f16_ss(d, a, bd, kIdescS, kk > 0);
+      for (int kk = 0; kk < T::D / 16; ++kk) {  // K-steps of 16 elements = 32 B
+        const uint64_t a = tc::smem_desc_sw128(q_addr + kk * 32, 16, 1024);
+        const uint64_t bd = tc::smem_desc_sw128(k_addr + kk * 32, 16, 1024);
+        if (leader) tc::mma_f16_ss(d, a, bd, kIdescS, kk > 0);
+      }
+      if (leader) tc::commit(&s_full[g]);
+      __syncwarp();
+    };
+    auto issue_o = [&](int g, int t) {  // W_g (+)= P_g(t) V_t
+      const int s = t % T::STAGES;
+      const uint32_t p_addr = ptx::smem_u32(smem + T::OFF_P + g * T::P_BYTES);
+      const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V + s * T::V_BYTES);
+      const uint32_t d = tmem + T::O_COL + g * 64;
+#pragma unroll
+      for (int kk = 0; kk < T::TK / 16; ++kk) {
+        // P: K-major, two 64-key chunks of 128 rows x 128 B
+        const uint32_t pa = p_addr + (kk >> 2) * (T::TQ * 128) + (kk & 3) * 32;
+        const uint64_t a = tc::smem_desc_sw128(pa, 16, 1024);
+        // V: MN-major (rows = keys, 128 B each); 16 keys per step = 2 swizzle atoms
+        const uint64_t bd = tc::smem_desc_sw128(v_addr + kk * 2048, 16, 1024);
+        if (leader) tc::mma_f16_ss(d, a, bd, kIdescO, (t > 0 || kk > 0) ? 1u : 0u);
+      }
+      if (leader) tc::commit(&o_full[g]);
+      __syncwarp();
+    };
+    // lane 0's view of a barrier phase, broadcast so the schedule stays uniform
+    auto ready = [&](uint64_t* bar, uint32_t parity) {
+      return __shfl_sync(0xffffffffu, ptx::mbar_test(bar, parity) ? 1 : 0, 0) != 0;
+    };
+    // Event loop over both groups: S_g(t+1) is issued as soon as group g
+    // has pulled S_g(t) into registers (s_free) — it overlaps the group's own
+    // exponentials — and P_g(t) V_t as soon as P_g(t) is written (p_full).
+    // Each barrier is only ever tested for its next phase, which cannot
+    // have been overtaken (every phase needs an MMA issued here first), and
+    // with test_wait: a try_wait could park the warp on one group's barrier
+    // while the other group's P is ready.
+    ptx::mbar_wait(qbar, 0);
+    int ns[GROUPS], npv[GROUPS];  // next S tile / next P V tile per group
+    for (int g = 0; g < GROUPS; ++g) ns[g] = npv[g] = 0;
+    int kv_released = 0;  // tiles whose K/V stage was handed back
+    while (kv_released < ntiles) {
+#pragma unroll
+      for (int g = 0; g < GROUPS; ++g) {
+        const int t = ns[g];
+        if (t < ntiles && (t == 0 || ready(&s_free[g], (t - 1) & 1)) &&
+            ready(&kv_full[t % T::STAGES], (t / T::STAGES) & 1)) {
+          tc::fence_after_sync();
+          if (lane == 0) TC_MARK(8 + g, t, 0);
+          issue_s(g, t);
+          ns[g] = t + 1;
         }
-        tc::commit(&s_full[g]);
-      };
-      auto issue_o = [&](int g, int t) {  // W_g (+)= P_g(t) V_t
-        const int s = t % T::STAGES;
-        const uint32_t p_addr = ptx::smem_u32(smem + T::OFF_P + g * T::P_BYTES);
-        const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V + s * T::V_BYTES);
-        const uint32_t d = tmem + T::O_COL + g * 64;
+        const int u = npv[g];
+        if (u < ns[g] && ready(&p_full[g], u & 1)) {
+          tc::fence_after_sync();
+          if (lane == 0) TC_MARK(8 + g, u, 1);
+          issue_o(g, u);
+          npv[g] = u + 1;
+          int done = npv[0];
 #pragma unroll
-        for (int kk = 0; kk < T::TK / 16; ++kk) {
-          // P: K-major, two 64-key chunks of 128 rows x 128 B
-          const uint32_t pa = p_addr + (kk >> 2) * (T::TQ * 128) + (kk & 3) * 32;
-          const uint64_t a = tc::smem_desc_sw128(pa, 16, 1024);
-          // V: MN-major (rows = keys, 128 B each); 16 keys per step = 2 swizzle atoms
-          const uint64_t bd = tc::smem_desc_sw128(v_addr + kk * 2048, 16, 1024);
-          tc::mma_f16_ss(d, a, bd, kIdescO, (t > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc::commit(&o_full[g]);
-      };
-      // Event loop over both groups: S_g(t+1) is issued as soon as group g
-      // has pulled S_g(t) into registers (s_free) — it overlaps the group's own
-      // exponentials — and P_g(t) V_t as soon as P_g(t) is written (p_full).
-      // Each barrier is only ever tested for its next phase, which cannot
-      // have been overtaken (every phase needs an MMA issued here first).
-      ptx::mbar_wait(qbar, 0);
-      int ns[GROUPS], npv[GROUPS];  // next S tile / next P V tile per group
-      for (int g = 0; g < GROUPS; ++g) ns[g] = npv[g] = 0;
-      int kv_released = 0;  // tiles whose K/V stage was handed back
-      while (kv_released < ntiles) {
-#pragma unroll
-        for (int g = 0; g < GROUPS; ++g) {
-          const int t = ns[g];
-          if (t < ntiles && (t == 0 || ptx::mbar_try_wait(&s_free[g], (t - 1) & 1)) &&
-              ptx::mbar_try_wait(&kv_full[t % T::STAGES], (t / T::STAGES) & 1)) {
-            tc::fence_after_sync();
-            issue_s(g, t);
-            ns[g] = t + 1;
-          }
-          const int u = npv[g];
-          if (u < ns[g] && ptx::mbar_try_wait(&p_full[g], u & 1)) {
-            tc::fence_after_sync();
-            issue_o(g, u);
-            npv[g] = u + 1;
-            int done = npv[0];
-#pragma unroll
-            for (int gg = 1; gg < GROUPS; ++gg) done = npv[gg] < done ? npv[gg] : done;
-            if (done > kv_released) {  // P V of tile kv_released issued for every group
-              tc::commit(&kv_empty[kv_released % T::STAGES]);
-              ++kv_released;
-            }
+          for (int gg = 1; gg < GROUPS; ++gg) done = npv[gg] < done ? npv[gg] : done;
+          if (done > kv_released) {  // P V of tile kv_released issued for every group
+            if (leader) tc::commit(&kv_empty[kv_released % T::STAGES]);
+            __syncwarp();
+            ++kv_released;
           }
         }
       }
@@ -247,7 +281,9 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     const uint32_t prow_s = ptx::smem_u32(smem + T::OFF_P + g * T::P_BYTES);
 
     for (int t = 0; t < ntiles; ++t) {
+      if (lane == 0) TC_MARK(warp, t, 0);
       ptx::mbar_wait(&s_full[g], t & 1);
+      if (lane == 0) TC_MARK(warp, t, 1);
       tc::fence_after_sync();
       float s[128];
 #pragma unroll
@@ -261,6 +297,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       // S_g(t) is in registers: the tensor core may overwrite it with S_g(t+1)
       tc::fence_before_sync();
       ptx::mbar_arrive(&s_free[g]);
+      if (lane == 0) TC_MARK(warp, t, 2);
       const int kv_hi = p.n_kv - t * T::TK;  // valid keys in this tile
       if (kv_hi < T::TK) {                   // tail tile (warp-uniform): mask past n_kv
 #pragma unroll
@@ -287,7 +324,9 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       m_run = m_new;
       // P_g(t-1) V done: the P tile is free and W_g holds tiles < t
       if (t > 0) {
+        if (lane == 0) TC_MARK(warp, t, 3);
         ptx::mbar_wait(&o_full[g], (t - 1) & 1);
+        if (lane == 0) TC_MARK(warp, t, 4);
         tc::fence_after_sync();
         if (__any_sync(0xffffffffu, move)) {  // rescale this warp's W rows in TMEM
 #pragma unroll
@@ -333,6 +372,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       ptx::fence_proxy_async_smem();
       tc::fence_before_sync();
       ptx::mbar_arrive(&p_full[g]);
+      if (lane == 0) TC_MARK(warp, t, 5);
     }
     // ---- epilogue: Y = W / S (engine.py:375-382) in the input's 16-bit format ----
     float w[64];
