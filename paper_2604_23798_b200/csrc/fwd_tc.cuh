@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     // Each barrier is only ever tested for its next phase, which cannot
     // have been overtaken (every phase needs an MMA issued here first), and
     // with test_wait: a try_wait could park the warp on one group's barrier
-    // while the other group's P is ready.
+    // while the other group's P is ready. (Probing all barriers at once with
+    // one ballot, PV before S, measured slower: 700 vs 769 TFLOP/s at 16K.)
     ptx::mbar_wait(qbar, 0);
     int ns[GROUPS], npv[GROUPS];  // next S tile / next P V tile per group
     for (int g = 0; g < GROUPS; ++g) ns[g] = npv[g] = 0;
@@ -304,18 +305,28 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
         for (int i = 0; i < 128; ++i)
           if (i >= kv_hi) s[i] = p.neg ? CUDART_INF_F : -CUDART_INF_F;
       }
-      // row max of the signed scores, in log2 units (warp-uniform sign branch)
+      // row max of the signed scores, in log2 units (warp-uniform sign branch;
+      // eight partial maxima keep the reduction off one dependent chain)
       float m_tile;
-      if (!p.neg) {
-        float mx = s[0];
+      {
+        float acc[8];
+        if (!p.neg) {
 #pragma unroll
-        for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
-        m_tile = mx * cs;
-      } else {
-        float mn = s[0];
+          for (int j = 0; j < 8; ++j) acc[j] = s[j];
 #pragma unroll
-        for (int i = 1; i < 128; ++i) mn = fminf(mn, s[i]);
-        m_tile = mn * cs;
+          for (int i = 8; i < 128; i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = fmaxf(acc[j], s[i + j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = -s[j];
+#pragma unroll
+          for (int i = 8; i < 128; i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = fmaxf(acc[j], -s[i + j]);
+        }
+        m_tile = fmaxf(fmaxf(fmaxf(acc[0], acc[1]), fmaxf(acc[2], acc[3])),
+                       fmaxf(fmaxf(acc[4], acc[5]), fmaxf(acc[6], acc[7]))) * c2;
       }
       // deferred anchor: move only when the tile max exceeds it by > kRescaleLog2
       const bool move = m_tile > m_run + kRescaleLog2;
