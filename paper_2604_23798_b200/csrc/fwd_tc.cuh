@@ -72,6 +72,39 @@ __device__ unsigned long long g_tc_trace[16 * kTcTraceTiles * 8];
   } while (0)
 #endif
 
+// Share of the exponentials computed on the FMA pipe instead of MUFU: this
+// many pairs out of every 8 scores (0..4). MUFU.EX2 issues at 16 lanes/clk/SM,
+// so with 128 exponentials per row per tile it is the softmax's binding
+// pipe; a polynomial on FFMA2 moves part of that load to the idle FMA pipe.
+#ifndef ELSA_TC_POLY_PAIRS
+#define ELSA_TC_POLY_PAIRS 0  // measured: 1 pair 699, 2 pairs 654 vs 0 763 TFLOP/s at 16K
+#endif
+constexpr int kTcPolyPairs = ELSA_TC_POLY_PAIRS;
+
+// 2^x for a pair, x <= 2^7, on the FMA pipe: x = j + f with j = rint(x) (the
+// 1.5*2^23 shifter), f in [-1/2, 1/2]; 2^f by its degree-4 Taylor polynomial
+// (relative error < 6e-5, below the 16-bit formats' rounding of P:
+// 2^-9 bf16, 2^-11 fp16); 2^j added to the exponent field. x is clamped to
+// -126 so the result stays normal (>= 0.7 * 2^-126: negligible against S >= 1).
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
+  using ptx::f32x2;
+  const f32x2 x = ptx::pack2(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const f32x2 shifter = ptx::pack2(12582912.f, 12582912.f);
+  const f32x2 r = ptx::fadd2(x, shifter);        // j in the low mantissa bits
+  const f32x2 j = ptx::fadd2(r, ptx::pack2(-12582912.f, -12582912.f));
+  const f32x2 f = ptx::ffma2r(j, ptx::pack2(-1.f, -1.f), x);  // x - j, exact
+  f32x2 q = ptx::ffma2r(f, ptx::pack2(9.6181291e-3f, 9.6181291e-3f),
+                        ptx::pack2(5.5504109e-2f, 5.5504109e-2f));
+  q = ptx::ffma2r(q, f, ptx::pack2(2.4022651e-1f, 2.4022651e-1f));
+  q = ptx::ffma2r(q, f, ptx::pack2(6.9314718e-1f, 6.9314718e-1f));
+  q = ptx::ffma2r(q, f, ptx::pack2(1.f, 1.f));
+  float q0, q1, r0, r1;
+  ptx::unpack2(q, q0, q1);
+  ptx::unpack2(r, r0, r1);
+  y0 = __int_as_float(__float_as_int(q0) + (__float_as_int(r0) << 23));
+  y1 = __int_as_float(__float_as_int(q1) + (__float_as_int(r1) << 23));
+}
+
 // anchor hysteresis of the deferred rescale (log2 units): P <= 2^8
 constexpr float kRescaleLog2 = 8.f;
 
@@ -359,7 +392,15 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       for (int u = 0; u < 16; ++u) {  // 16-byte units of 8 keys
         float pv[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) pv[e] = ptx::ex2(fmaf(s[u * 8 + e], cs, neg_m));
+        for (int e = 0; e < 8; e += 2) {
+          const float x0 = fmaf(s[u * 8 + e], cs, neg_m), x1 = fmaf(s[u * 8 + e + 1], cs, neg_m);
+          if (e < 2 * kTcPolyPairs) {  // this pair on the FMA pipe, the rest on MUFU
+            ex2_poly2(x0, x1, pv[e], pv[e + 1]);
+          } else {
+            pv[e] = ptx::ex2(x0);
+            pv[e + 1] = ptx::ex2(x1);
+          }
+        }
         ps0 += (pv[0] + pv[1]) + (pv[2] + pv[3]);
         ps1 += (pv[4] + pv[5]) + (pv[6] + pv[7]);
         uint4 pk;
