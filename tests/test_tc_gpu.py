@@ -59,3 +59,32 @@ def test_tc_rejects_other_head_dims():
     q = torch.randn(1, 1, 16, 32, device=DEV, dtype=torch.bfloat16)
     with pytest.raises(elsa.ShapeError):
         elsa.scaled_dot_product_attention(q, q, q)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_tc_two_tile_ctas_ragged(dtype):
+    # >= one wave of two-query-tile CTAs: the ping-pong (two softmax warpgroups)
+    # kernel, with ragged n_q (partial second tile) and a ragged key tail
+    _check(dtype, 2, 8, 4096 + 77, 1000, seed=41)
+
+
+def test_tc_deferred_anchor_moves():
+    # logits that grow along the key axis: every tile raises the row maximum
+    # by more than the 2^8 hysteresis, so the W rows in TMEM are rescaled
+    # (the rare path of the deferred anchor) tile after tile
+    g = torch.Generator(device=DEV)
+    g.manual_seed(7)
+    B, H, n = 2, 8, 4096
+    q = torch.randn(B, H, n, 64, device=DEV, generator=g)
+    k = torch.randn(B, H, n, 64, device=DEV, generator=g)
+    ramp = torch.linspace(0.2, 3.0, n, device=DEV).view(1, 1, n, 1)
+    k = (k * ramp + ramp * 2.0).to(torch.bfloat16)
+    q = (q.abs() + 0.5).to(torch.bfloat16)
+    v = torch.randn(B, H, n, 64, device=DEV, generator=g).to(torch.bfloat16)
+    y = elsa.scaled_dot_product_attention(q, k, v, check_numerics=True)
+    ref = oracle.naive_attention(*(t.double().cpu().numpy() for t in (q, k, v)))
+    ours = oracle.row_rel_err(y.double().cpu().numpy(), ref)
+    theirs = oracle.row_rel_err(torch.nn.functional.scaled_dot_product_attention(
+        q, k, v).double().cpu().numpy(), ref)
+    assert np.percentile(ours, 99) <= max(2 * np.percentile(theirs, 99), 2.0 ** -8)
+    assert ours.max() <= max(2 * theirs.max(), 2.0 ** -7)
