@@ -275,16 +275,8 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     while (kv_released < ntiles) {
 #pragma unroll
       for (int g = 0; g < GROUPS; ++g) {
-        const int t = ns[g];
-        if (t < ntiles && (t == 0 || ready(&s_free[g], (t - 1) & 1)) &&
-            ready(&kv_full[t % T::STAGES], (t / T::STAGES) & 1)) {
-          tc::fence_after_sync();
-          if (lane == 0) TC_MARK(8 + g, t, 0);
-          issue_s(g, t);
-          ns[g] = t + 1;
-        }
         const int u = npv[g];
-        if (u < ns[g] && ready(&p_full[g], u & 1)) {
+        if (u < ns[g] && ready(&p_full[g], u & 1)) {  // P V first: on the softmax's path
           tc::fence_after_sync();
           if (lane == 0) TC_MARK(8 + g, u, 1);
           issue_o(g, u);
@@ -297,6 +289,14 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
             __syncwarp();
             ++kv_released;
           }
+        }
+        const int t = ns[g];
+        if (t < ntiles && (t == 0 || ready(&s_free[g], (t - 1) & 1)) &&
+            ready(&kv_full[t % T::STAGES], (t / T::STAGES) & 1)) {
+          tc::fence_after_sync();
+          if (lane == 0) TC_MARK(8 + g, t, 0);
+          issue_s(g, t);
+          ns[g] = t + 1;
         }
       }
     }
