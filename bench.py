@@ -66,6 +66,12 @@ def parse():
     ap.add_argument("--cpu-sample-tiles", type=int, default=0,
                     help="64-query tiles per CPU sample (0 = one per worker)")
     ap.add_argument("--cpu-workers", type=int, default=0)
+    ap.add_argument("--dist-path", action="store_true",
+                    help="run the KV-sharded multi-GPU code path even at N = 1 (a world-size-1 "
+                         "NCCL group; checks the N > 1 path on a single GPU)")
+    ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: state exchange + merge over symmetric peer memory (one "
+                         "kernel) or NCCL all_to_all + merge kernel")
     return ap.parse_args()
 
 
@@ -226,8 +232,13 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.dist_path:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
+    sharded = world > 1 or args.dist_path
     B, H, n = args.batch, args.heads, args.n
     fl = flops(B, H, n, n)
     stream = torch.cuda.current_stream(dev)
@@ -239,23 +250,40 @@ def main():
     k = torch.randn(B, H, n, 64, device=dev, generator=gen)
     v = torch.randn(B, H, n, 64, device=dev, generator=gen)
     chunks = 8 if world <= 8 and 8 % world == 0 else world
-    if world > 1:
+    if sharded:
         k_loc, v_loc, off = edist.shard_kv(k, v, rank, world, chunks)
         k_loc, v_loc = k_loc.contiguous(), v_loc.contiguous()
 
     launches = [0]
+    exchange = [args.exchange]
 
     def step():
-        if world == 1:
+        if not sharded:
             y = elsa.scaled_dot_product_attention(q, k, v)
             launches[0] += elsa.last_launch_count()
             return y
-        r = edist.kv_sharded_attention(q, k_loc, v_loc, off, n, chunks=chunks, gather=False)
+        r = edist.kv_sharded_attention(q, k_loc, v_loc, off, n, chunks=chunks, gather=False,
+                                       exchange=exchange[0])
         launches[0] += 2 * (chunks // world) + 1
         return r
 
+    if sharded and exchange[0] == "peer":
+        # the symmetric-memory rendezvous needs peer access between every pair
+        # of GPUs; if this node cannot provide it, measure the NCCL exchange
+        try:
+            step()
+            torch.cuda.synchronize()
+            ok = torch.ones(1, device=dev)
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] peer exchange unavailable ({str(exc)[:120]}); using NCCL",
+                  file=sys.stderr)
+            ok = torch.zeros(1, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() < 1:
+            exchange[0] = "nccl"
+
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier()
 
     for _ in range(max(args.warmup, 3)):
@@ -279,7 +307,7 @@ def main():
     ms_total = e0.elapsed_time(e1)
     clock_info = clocks.stop()
     timed_launches = launches[0]
-    if world > 1:
+    if sharded:
         t = torch.tensor([ms_total], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
@@ -288,7 +316,7 @@ def main():
 
     # ---- e2e through the public API with pinned host buffers ----
     e2e = None
-    if not args.no_e2e and world > 1:
+    if not args.no_e2e and sharded:
         # each rank: H2D of Q and its K/V shard, the KV-sharded forward, D2H of
         # its Y row slice (the ranks' slices together are the whole Y)
         hq = q.cpu().pin_memory()
@@ -300,7 +328,8 @@ def main():
             dq.copy_(hq, non_blocking=True)
             dk.copy_(hk, non_blocking=True)
             dv_.copy_(hv, non_blocking=True)
-            _, yr = edist.kv_sharded_attention(dq, dk, dv_, off, n, chunks=chunks, gather=False)
+            _, yr = edist.kv_sharded_attention(dq, dk, dv_, off, n, chunks=chunks, gather=False,
+                                               exchange=exchange[0])
             if hy[0] is None:
                 hy[0] = torch.empty(yr.shape, dtype=yr.dtype).pin_memory()
             hy[0].copy_(yr, non_blocking=True)
@@ -325,7 +354,7 @@ def main():
                "d2h_bytes_per_step": hy[0].numel() * 4 * world, "steps": steps_e2e,
                "api": "paper_2604_23798_b200.dist.kv_sharded_attention per rank, pinned host "
                       "buffers (bytes summed over ranks; max-over-ranks time)"}
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not sharded:
         hq = q.cpu().pin_memory()
         hk = k.cpu().pin_memory()
         hv = v.cpu().pin_memory()
@@ -372,14 +401,14 @@ def main():
         "k4_ffma_measured": k4, "frac_of_k4": (value / k4) if k4 else None,
         "traffic": traffic, "traffic_workload": traffic_workload,
         "algorithmic_bytes_per_launch": 4 * B * H * (n * 64 * 3 + n * 64),
-        "kernel": "elsa::fwd_f32_kernel (" + elsa.describe_plan(q, k, v) + ")" if world == 1 else "elsa::fwd_f32_kernel",
+        "kernel": "elsa::fwd_f32_kernel (" + elsa.describe_plan(q, k, v) + ")" if not sharded else "elsa::fwd_f32_kernel",
         "measurement": "CUDA events on the launching stream around the K timed steps; "
                        "one kernel launch per step at this shape",
     }
 
     # ---- sweep (kernel-only: CUDA-graph replays, L2 flushed between them) ----
     sweep = []
-    if not args.no_sweep and world == 1:
+    if not args.no_sweep and not sharded:
         flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
         cases = [(1, 16, nn) for nn in (1024, 2048, 4096, 8192, 16384)] + [(8, 12, 512), (1, 1, 1024)]
         for (bb, hh, nn) in cases:
@@ -436,7 +465,7 @@ def main():
 
     # ---- CPU baseline: the reference's algorithm on the host cores (rank 0, N=1) ----
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not sharded and not args.no_cpu_baseline:
         workers = _cpu_workers(args)
         tiles = args.cpu_sample_tiles or workers
         val, secs, desc = cpu_baseline_sample(n, H, B, tiles, workers)
@@ -451,16 +480,17 @@ def main():
             "data": "synthetic N(0,1) Q/K/V (torch.randn), resident in HBM",
             "config": {"workload": f"C3 FP32 attention B{B} H{H} n{n} d64 dv64"
                                    + (f", KV-sharded over {world} GPUs ({chunks} chunks)"
-                                      if world > 1 else ""),
+                                      if sharded else ""),
                        "B": B, "H": H, "n": n, "d": 64, "dv": 64,
                        "l2": "inputs 3x%.0f MB > 126 MB L2; sweep flushes L2 (256 MB write) "
                              "between timed iterations" % (q.numel() * 4 / 1e6),
-                       "parallelism": f"kv-shard{world}" if world > 1 else "single GPU"},
+                       "parallelism": f"kv-shard{world}" if sharded else "single GPU",
+                       "exchange": exchange[0] if sharded else None},
             "e2e": e2e, "gpu_launches": timed_launches, "clocks": clock_info,
             "roofline": roofline, "cpu_baseline": cpu, "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 

@@ -142,6 +142,19 @@ int elsa_merge_f32(const float* m, const float* S, const float* W,
                    int finalize, float* y, float* m_out, float* S_out,
                    float* W_out, void* stream);
 
+/* Fused exchange + merge for the KV-sharded multi-GPU path:
+ * rank r's m/S/W buffers (peer-mapped device pointers, e.g. symmetric memory
+ * over NVLink) hold the natural-log states of its per_rank key chunks for all
+ * rows_total query rows ([chunk][row], W [chunk][row][dv]); this merges rows
+ * [row_lo, row_lo + rows) over all ranks * per_rank chunks in global chunk
+ * order (chunk c = rank c / per_rank, local chunk c % per_rank) with the
+ * merge_tree shape and writes y[rows][dv] = W / S. ranks <= 16,
+ * ranks * per_rank <= 32. Replaces all_to_all + elsa_merge_f32. */
+int elsa_merge_peers_f32(const float* const* m_ptrs, const float* const* S_ptrs,
+                         const float* const* W_ptrs, int ranks, int per_rank,
+                         int64_t rows_total, int64_t row_lo, int64_t rows, int dv,
+                         float* y, void* stream);
+
 /* Per-key-block partial states for every query row:
  * block j covers keys [j*block_size, min((j+1)*block_size, n_kv)); natural-log
  * anchors. Layout, nblocks = ceil(n_kv / block_size), rows = B*H*n_q in

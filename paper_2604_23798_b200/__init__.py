@@ -23,6 +23,7 @@ from .attention import (  # noqa: F401
     describe_plan,
     ffma_peak_tflops,
     last_launch_count,
+    merge_peer_states,
     merge_states,
     partial_states,
     resolve_kv_splits,

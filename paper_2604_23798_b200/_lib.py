@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "elsa_partial_f32",
     "elsa_fwd_f16",
     "elsa_merge_f32",
+    "elsa_merge_peers_f32",
     "elsa_blockwise_f32",
     "elsa_block_scan_workspace_bytes",
     "elsa_block_scan_f32",
@@ -103,6 +104,10 @@ def _declare(h):
     h.elsa_merge_f32.restype = c_int
     h.elsa_merge_f32.argtypes = [c_vp, c_vp, c_vp, c_int, c_i64, c_int, c_i64, c_int,
                                  c_vp, c_vp, c_vp, c_vp, c_vp]
+    h.elsa_merge_peers_f32.restype = c_int
+    h.elsa_merge_peers_f32.argtypes = [ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
+                                       ctypes.POINTER(c_vp), c_int, c_int, c_i64, c_i64, c_i64,
+                                       c_int, c_vp, c_vp]
     h.elsa_blockwise_f32.restype = c_int
     h.elsa_blockwise_f32.argtypes = [c_vp, c_vp, c_vp, shp, c_dbl, c_i64, c_vp, c_vp, c_vp, c_vp]
     h.elsa_block_scan_workspace_bytes.restype = c_sz

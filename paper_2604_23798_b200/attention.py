@@ -29,6 +29,7 @@ __all__ = [
     "attention_from_host",
     "partial_states",
     "merge_states",
+    "merge_peer_states",
     "blockwise_states",
     "inter_block_combine",
     "check_device_error",
@@ -329,13 +330,16 @@ def _sdpa_tc(q, k, v, sc, out):
     return y
 
 
-def partial_states(query, key, value, kv_begin=0, kv_end=None, scale=None, kv_splits=1):
+def partial_states(query, key, value, kv_begin=0, kv_end=None, scale=None, kv_splits=1, *,
+                   out=None):
     """The (m, S, W) summary of keys ``[kv_begin, kv_end)`` for every query —
     the per-chunk state of Proposition 1, as
     ``engine.blockwise_states`` + ``inter_block_combine`` produce on CPU
     (engine.py:430-451, 265-297). Returns ``m, S`` shaped (B, H, n_q) and
     ``W`` shaped (B, H, n_q, dv); ``m`` is in natural-log units, -inf for an
-    empty range."""
+    empty range. ``out=(m, S, W)``: dense float32 CUDA tensors with
+    B*H*n_q and B*H*n_q*dv elements to write into (e.g. views of a
+    peer-mapped buffer)."""
     _validate(query, key, value)
     q, k, v = (_prep(_as_4d(t, n)) for t, n in ((query, "query"), (key, "key"), (value, "value")))
     B, H, n_q, d = q.shape
@@ -343,9 +347,18 @@ def partial_states(query, key, value, kv_begin=0, kv_end=None, scale=None, kv_sp
     kv_end = n_kv if kv_end is None else int(kv_end)
     sc = (1.0 / math.sqrt(d)) if scale is None else float(scale)
     shp = _shape(q, k, v)
-    m = torch.empty((B, H, n_q), device=q.device, dtype=torch.float32)
-    S = torch.empty_like(m)
-    W = torch.empty((B, H, n_q, dv), device=q.device, dtype=torch.float32)
+    if out is None:
+        m = torch.empty((B, H, n_q), device=q.device, dtype=torch.float32)
+        S = torch.empty_like(m)
+        W = torch.empty((B, H, n_q, dv), device=q.device, dtype=torch.float32)
+    else:
+        m, S, W = out
+        rows = B * H * n_q
+        for name, t, numel in (("m", m, rows), ("S", S, rows), ("W", W, rows * dv)):
+            if (t.dtype != torch.float32 or t.device != q.device or not t.is_contiguous()
+                    or t.numel() != numel):
+                raise ShapeError(f"out {name} must be a contiguous float32 tensor of {numel} "
+                                 "elements on the input device")
     h = _lib.lib()
     with torch.cuda.device(q.device):
         # workspace for the internal split tree, sized for the requested count
@@ -402,6 +415,24 @@ def merge_states(m, S, W, finalize=True):
             ctypes.c_void_p(Wo.data_ptr()), _stream_ptr(m.device))
         _lib.check_status(st, "elsa_merge_f32")
         return mo, So, Wo
+
+
+def merge_peer_states(m_ptrs, S_ptrs, W_ptrs, per_rank, rows_total, row_lo, rows, dv, device=None):
+    """Fused exchange + merge of the KV-sharded path (``elsa_merge_peers_f32``):
+    rank r's state arrays live at the device pointers ``m_ptrs[r]``, ... (peer
+    mapped, e.g. symmetric memory); returns Y for rows [row_lo, row_lo + rows)
+    merged over all ranks' chunks in global chunk order."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    ranks = len(m_ptrs)
+    arr = ctypes.c_void_p * ranks
+    y = torch.empty((rows, dv), device=dev, dtype=torch.float32)
+    with torch.cuda.device(dev):
+        st = _lib.lib().elsa_merge_peers_f32(
+            arr(*m_ptrs), arr(*S_ptrs), arr(*W_ptrs), int(ranks), int(per_rank),
+            int(rows_total), int(row_lo), int(rows), int(dv), ctypes.c_void_p(y.data_ptr()),
+            _stream_ptr(dev))
+        _lib.check_status(st, "elsa_merge_peers_f32")
+    return y
 
 
 def blockwise_states(query, key, value, block_size=128, scale=None):

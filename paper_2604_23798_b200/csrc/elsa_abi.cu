@@ -880,6 +880,48 @@ int elsa_merge_f32(const float* m, const float* S, const float* W, int parts, in
   return launch_merge(mp, static_cast<cudaStream_t>(stream));
 }
 
+int elsa_merge_peers_f32(const float* const* m_ptrs, const float* const* S_ptrs,
+                         const float* const* W_ptrs, int ranks, int per_rank, int64_t rows_total,
+                         int64_t row_lo, int64_t rows, int dv, float* y, void* stream) {
+  t_last_launches = 0;
+  if (!m_ptrs || !S_ptrs || !W_ptrs || !y) return ELSA_ERR_SHAPE;
+  if (ranks < 1 || ranks > kMaxPeers || per_rank < 1 || ranks * per_rank > kMergeMaxParts)
+    return ELSA_ERR_SHAPE;
+  if (dv < 1 || dv > 64 || rows < 0 || row_lo < 0 || rows_total < row_lo + rows) return ELSA_ERR_SHAPE;
+  if (rows == 0) return ELSA_OK;
+  DeviceCache* dc = nullptr;
+  if (int st = current_device_cache(&dc)) return st;
+  PeerMergeParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  for (int r = 0; r < ranks; ++r) {
+    if (!m_ptrs[r] || !S_ptrs[r] || !W_ptrs[r]) return ELSA_ERR_SHAPE;
+    mp.m[r] = m_ptrs[r];
+    mp.S[r] = S_ptrs[r];
+    mp.W[r] = W_ptrs[r];
+  }
+  mp.ranks = ranks;
+  mp.per_rank = per_rank;
+  mp.rows_total = rows_total;
+  mp.row_lo = row_lo;
+  mp.rows = rows;
+  mp.dv = dv;
+  mp.y = y;
+  mp.err = dc->err;
+  constexpr int kWarps = 8;
+  const int64_t blocks = ceil_div(rows, kWarps);
+  if (blocks >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
+  const int parts = ranks * per_rank;
+  auto kern = parts <= 2    ? merge_peers_kernel<2>
+              : parts <= 4  ? merge_peers_kernel<4>
+              : parts <= 8  ? merge_peers_kernel<8>
+              : parts <= 16 ? merge_peers_kernel<16>
+                            : merge_peers_kernel<32>;
+  kern<<<unsigned(blocks), kWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(mp);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "peer merge launch");
+  ++t_last_launches;
+  return ELSA_OK;
+}
+
 int elsa_blockwise_f32(const float* q, const float* k, const float* v, const elsa_shape* shp,
                        double scale, int64_t block_size, float* m, float* S, float* W,
                        void* stream) {

@@ -26,6 +26,13 @@ G = 1, 2, 4, 8 (the merge tree has the same C leaves in the same order).
 The compute and merge steps are injectable (``partial_fn``, ``merge_fn``) so
 the host logic — chunk plan, packing, exchange, tree order — is covered by
 world-size-2 ``gloo`` tests on CPU; the product path uses libelsa kernels.
+
+``exchange="peer"`` replaces steps 2-3 with one kernel: each rank writes its
+chunk states into a symmetric (peer-mapped, NVLink) buffer
+(``torch.distributed._symmetric_memory``), a device-side barrier orders the
+ranks, and ``elsa_merge_peers_f32`` reads every rank's states for its row
+slice straight from peer memory and merges them in registers — no
+all_to_all, no staging copy, bitwise identical to the NCCL exchange.
 """
 
 from __future__ import annotations
@@ -81,8 +88,48 @@ def _gpu_merge(m, S, W):
     return merge_states(m, S, W, finalize=True)
 
 
+_PEER_BUFS = {}
+
+
+def _peer_buffer(per, rows, dv, device, group):
+    """Symmetric state buffer [m | S | W] for (per, rows, dv), rendezvoused once
+    per shape and group and reused (the trailing barrier of every call keeps
+    reuse safe)."""
+    import torch.distributed._symmetric_memory as symm_mem
+
+    key = (per, rows, dv, device.index, id(group))
+    hit = _PEER_BUFS.get(key)
+    if hit is None:
+        n = per * rows * (2 + dv)
+        buf = symm_mem.empty(n, dtype=torch.float32, device=device)
+        grp = group if group is not None else dist.group.WORLD
+        hdl = symm_mem.rendezvous(buf, grp)
+        hit = (buf, hdl)
+        _PEER_BUFS[key] = hit
+    return hit
+
+
+def _peer_exchange_merge(q, states_fn, per, rows, dv, chunks, group, rank, world):
+    buf, hdl = _peer_buffer(per, rows, dv, q.device, group)
+    m = buf[: per * rows].view(per, rows)
+    S = buf[per * rows: 2 * per * rows].view(per, rows)
+    W = buf[2 * per * rows:].view(per, rows, dv)
+    states_fn(m, S, W)
+    hdl.barrier(channel=0)  # every rank's states written (device-side, stream-ordered)
+    lo, hi = row_slices(rows, world)[rank]
+    base = [int(p) for p in hdl.buffer_ptrs]
+    mp = [b for b in base]
+    Sp = [b + per * rows * 4 for b in base]
+    Wp = [b + 2 * per * rows * 4 for b in base]
+    from .attention import merge_peer_states
+    y_rows = merge_peer_states(mp, Sp, Wp, per, rows, lo, hi - lo, dv, device=q.device)
+    hdl.barrier(channel=1)  # peers finished reading before the buffer is rewritten
+    return lo, y_rows
+
+
 def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
-                         chunks=DEFAULT_CHUNKS, gather=True, partial_fn=None, merge_fn=None):
+                         chunks=DEFAULT_CHUNKS, gather=True, partial_fn=None, merge_fn=None,
+                         exchange="nccl"):
     """Exact attention with keys sharded across the ranks of ``group``.
 
     ``q``: full (B, H, n_q, d) on this rank; ``k_local``/``v_local``: this
@@ -91,6 +138,7 @@ def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
     Y (B, H, n_q, dv) when ``gather`` else ``(row_begin, Y_rows)`` for this
     rank's row slice (rows ordered (b, h, q)).
     """
+    injected = partial_fn is not None or merge_fn is not None
     partial_fn = partial_fn or _gpu_partial
     merge_fn = merge_fn or _gpu_merge
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -103,6 +151,36 @@ def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
     per = len(own)
     if kv_offset != bounds[own[0]][0] or kv_offset + k_local.shape[2] != bounds[own[-1]][1]:
         raise ShapeError("local K/V rows do not match this rank's chunk range")
+
+    if exchange == "peer":
+        if injected:
+            raise ShapeError("the peer exchange runs the libelsa kernels only")
+        if chunks > 32 or world > 16:
+            raise ShapeError("the peer merge handles <= 32 chunks over <= 16 ranks")
+
+        def states_fn(m, S, W):
+            from .attention import partial_states
+            for i, c in enumerate(own):
+                lo, hi = bounds[c]
+                partial_states(q, k_local, v_local, lo - kv_offset, hi - kv_offset, kv_splits=0,
+                               out=(m[i], S[i], W[i]))
+
+        my_lo, y_rows = _peer_exchange_merge(q, states_fn, per, rows, dv, chunks, group, rank,
+                                             world)
+        if not gather:
+            return my_lo, y_rows
+        slices = row_slices(rows, world)
+        if world == 1:
+            return y_rows.reshape(B, H, n_q, dv)
+        maxr = max(hi - lo for lo, hi in slices)
+        pad = torch.zeros((maxr, dv), dtype=torch.float32, device=q.device)
+        pad[: y_rows.shape[0]] = y_rows
+        outs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(outs, pad, group=group)
+        y = torch.cat([o[: hi - lo] for o, (lo, hi) in zip(outs, slices)])
+        return y.reshape(B, H, n_q, dv)
+    if exchange != "nccl":
+        raise ShapeError(f"exchange must be 'nccl' or 'peer', got {exchange!r}")
 
     # 1. per-chunk states, packed [chunk][row][2 + dv]
     states = torch.empty((per, rows, 2 + dv), dtype=torch.float32, device=q.device)

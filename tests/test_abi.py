@@ -136,3 +136,16 @@ def test_host_entry_validates_before_touching_the_device():
     s = _shape(2, 3, 128, 128)
     assert h.elsa_fwd_f32_host(None, p, p, p, ctypes.byref(s), 0.125, 0, None, 0, None) == 2
     assert h.elsa_fwd_f32_host(p, p, p, p, ctypes.byref(s), float("nan"), 0, None, 0, None) == 2
+
+
+def test_peer_merge_validates_before_touching_the_device():
+    h = _lib.lib()
+    buf = (ctypes.c_float * 4)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    arr = (ctypes.c_void_p * 1)(p)
+    y = p
+    # 33 chunks > the 32-leaf tree; 0 ranks; rows past rows_total; missing pointers
+    assert h.elsa_merge_peers_f32(arr, arr, arr, 1, 33, 4, 0, 4, 64, y, None) == 2
+    assert h.elsa_merge_peers_f32(arr, arr, arr, 0, 1, 4, 0, 4, 64, y, None) == 2
+    assert h.elsa_merge_peers_f32(arr, arr, arr, 1, 8, 4, 2, 4, 64, y, None) == 2
+    assert h.elsa_merge_peers_f32(None, arr, arr, 1, 8, 4, 0, 4, 64, y, None) == 2

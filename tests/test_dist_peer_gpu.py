@@ -1,0 +1,54 @@
+"""The fused peer-memory exchange of the KV-sharded path on one GPU (world
+size 1: the rank reads its own symmetric buffer through the same peer
+pointers a multi-GPU run uses): bitwise equal to the NCCL all_to_all path and
+within the FP64 bound."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+
+import paper_2604_23798_b200 as elsa  # noqa: E402
+from paper_2604_23798_b200 import dist as edist  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="module")
+def pg():
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(DEV)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    yield dist.group.WORLD
+
+
+@pytest.mark.parametrize("B,H,n,chunks", [(1, 4, 1000, 8), (2, 3, 513, 4), (1, 2, 4096, 8)])
+def test_peer_exchange_matches_nccl_and_oracle(pg, B, H, n, chunks):
+    Q, K, V = oracle.generate(31, "regular", b=B, h=H, n=n, d=64, d_v=64, dtype=np.float32)
+    q, k, v = (torch.from_numpy(x).to(DEV) for x in (Q, K, V))
+    kl, vl, off = edist.shard_kv(k, v, 0, 1, chunks)
+    y_nccl = edist.kv_sharded_attention(q, kl, vl, off, n, chunks=chunks, exchange="nccl")
+    y_peer = edist.kv_sharded_attention(q, kl, vl, off, n, chunks=chunks, exchange="peer")
+    y_again = edist.kv_sharded_attention(q, kl, vl, off, n, chunks=chunks, exchange="peer")
+    elsa.check_device_error(DEV)
+    assert torch.equal(y_nccl, y_peer) and torch.equal(y_peer, y_again)
+    err = oracle.row_rel_err(y_peer.cpu().numpy(), oracle.naive_attention(Q, K, V))
+    assert err.max() <= oracle.bound_threshold(n)
+    lo, rows = edist.kv_sharded_attention(q, kl, vl, off, n, chunks=chunks, exchange="peer",
+                                          gather=False)
+    assert lo == 0 and torch.equal(rows, y_peer.reshape(-1, 64))
