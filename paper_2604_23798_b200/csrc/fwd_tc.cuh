@@ -138,8 +138,9 @@ struct TcTraits {
   static constexpr int SOFTMAX_REGS = 232, OTHER_REGS = 40;
   static_assert(!kRegSplit || 2 * (SOFTMAX_REGS - 168) <= 168 - OTHER_REGS, "setmaxnreg budget");
   static constexpr uint32_t TMEM_COLS = GROUPS == 1 ? 256 : 512;
-  static constexpr uint32_t S_COL = 0;    // group g: S at 128 g
-  static constexpr uint32_t O_COL = 256;  // group g: W (P V accumulator) at 256 + 64 g
+  static constexpr uint32_t S_COL = 0;             // group g: S at 128 g
+  static constexpr uint32_t O_COL = 128 * GROUPS;  // group g: W (P V accumulator) at O_COL + 64 g
+  static_assert(O_COL + 64 * GROUPS <= TMEM_COLS, "TMEM columns");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
