@@ -116,12 +116,10 @@ struct TcTraits {
   static constexpr int Q_BYTES = TQ * ROW_BYTES;             // 16 KB per group
   static constexpr int K_BYTES = TK * ROW_BYTES;             // 16 KB
   static constexpr int V_BYTES = TK * ROW_BYTES;             // 16 KB
-  static constexpr int P_BYTES = TQ * TK * 2;                // 32 KB per group (two 64-key chunks)
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + GROUPS * Q_BYTES;
   static constexpr int OFF_V = OFF_K + STAGES * K_BYTES;
-  static constexpr int OFF_P = OFF_V + STAGES * V_BYTES;
-  static constexpr int OFF_BAR = OFF_P + GROUPS * P_BYTES;
+  static constexpr int OFF_BAR = OFF_V + STAGES * V_BYTES;
   // barriers: qbar, kv_full[3], kv_empty[3], s_full[G], s_free[G], p_full[G], o_full[G],
   // + tmem base word
   static constexpr int NBAR = 1 + 2 * STAGES + 4 * GROUPS;
@@ -140,7 +138,10 @@ struct TcTraits {
   static constexpr uint32_t TMEM_COLS = GROUPS == 1 ? 256 : 512;
   static constexpr uint32_t S_COL = 0;             // group g: S at 128 g
   static constexpr uint32_t O_COL = 128 * GROUPS;  // group g: W (P V accumulator) at O_COL + 64 g
-  static_assert(O_COL + 64 * GROUPS <= TMEM_COLS, "TMEM columns");
+  // group g: P (16-bit, two per 32-bit column) at P_COL + 64 g — the A operand
+  // of P V read straight from TMEM (no shared-memory round trip)
+  static constexpr uint32_t P_COL = 192 * GROUPS;
+  static_assert(P_COL + 64 * GROUPS <= TMEM_COLS, "TMEM columns");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
@@ -240,19 +241,16 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       if (leader) tc::commit(&s_full[g]);
       __syncwarp();
     };
-    auto issue_o = [&](int g, int t) {  // W_g (+)= P_g(t) V_t
+    auto issue_o = [&](int g, int t) {  // W_g (+)= P_g(t) V_t, P from TMEM
       const int s = t % T::STAGES;
-      const uint32_t p_addr = ptx::smem_u32(smem + T::OFF_P + g * T::P_BYTES);
       const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V + s * T::V_BYTES);
       const uint32_t d = tmem + T::O_COL + g * 64;
+      const uint32_t pa = tmem + T::P_COL + g * 64;
 #pragma unroll
       for (int kk = 0; kk < T::TK / 16; ++kk) {
-        // P: K-major, two 64-key chunks of 128 rows x 128 B
-        const uint32_t pa = p_addr + (kk >> 2) * (T::TQ * 128) + (kk & 3) * 32;
-        const uint64_t a = tc::smem_desc_sw128(pa, 16, 1024);
         // V: MN-major (rows = keys, 128 B each); 16 keys per step = 2 swizzle atoms
         const uint64_t bd = tc::smem_desc_sw128(v_addr + kk * 2048, 16, 1024);
-        if (leader) tc::mma_f16_ss(d, a, bd, kIdescO, (t > 0 || kk > 0) ? 1u : 0u);
+        if (leader) tc::mma_f16_ts(d, pa + kk * 8, bd, kIdescO, (t > 0 || kk > 0) ? 1u : 0u);
       }
       if (leader) tc::commit(&o_full[g]);
       __syncwarp();
@@ -313,7 +311,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     const float cs = p.neg ? -c2 : c2;  // exponent = s_raw * cs - m
     float m_run = -CUDART_INF_F;        // log2-domain anchor
     float l_run = 0.f;
-    const uint32_t prow_s = ptx::smem_u32(smem + T::OFF_P + g * T::P_BYTES);
+    const uint32_t p_tm = tmem + lane_base + T::P_COL + g * 64;
 
     for (int t = 0; t < ntiles; ++t) {
       if (lane == 0) TC_MARK(warp, t, 0);
@@ -394,6 +392,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       const ptx::f32x2 cs2 = ptx::pack2(cs, cs), nm2 = ptx::pack2(neg_m, neg_m);
       ptx::f32x2 psa = 0ull, psb = 0ull;
       float ps0 = 0.f, ps1 = 0.f;
+      uint32_t pk[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) {  // 16-byte units of 8 keys
         float pv[8];
@@ -420,22 +419,14 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
           ps0 += (pv[0] + pv[1]) + (pv[2] + pv[3]);
           ps1 += (pv[4] + pv[5]) + (pv[6] + pv[7]);
         }
-        uint4 pk;
-        if constexpr (kBF16) {
-          pk.x = tc::pack_bf16x2(pv[0], pv[1]);
-          pk.y = tc::pack_bf16x2(pv[2], pv[3]);
-          pk.z = tc::pack_bf16x2(pv[4], pv[5]);
-          pk.w = tc::pack_bf16x2(pv[6], pv[7]);
-        } else {
-          pk.x = tc::pack_f16x2(pv[0], pv[1]);
-          pk.y = tc::pack_f16x2(pv[2], pv[3]);
-          pk.z = tc::pack_f16x2(pv[4], pv[5]);
-          pk.w = tc::pack_f16x2(pv[6], pv[7]);
-        }
-        const int chunk = u >> 3;              // 64-key chunk
-        const int unit = (u & 7) ^ (row & 7);  // 128B swizzle: 16-B unit XOR row phase
-        ptx::sts128(prow_s + chunk * (T::TQ * 128) + row * 128 + unit * 16, pk);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          pk[(u & 3) * 4 + e] = kBF16 ? tc::pack_bf16x2(pv[2 * e], pv[2 * e + 1])
+                                      : tc::pack_f16x2(pv[2 * e], pv[2 * e + 1]);
+        if ((u & 3) == 3)  // 32 keys = 16 columns packed: into TMEM
+          tc::tmem_st_32x32b_x16(p_tm + (u >> 2) * 16, pk);
       }
+      tc::tmem_wait_st();
       float psum;
       if constexpr (GROUPS == 1) {
         const ptx::f32x2 pt = ptx::fadd2(psa, psb);
@@ -444,8 +435,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
         psum = ps0 + ps1;
       }
       l_run = fmaf(l_run, corr, psum);
-      // P_t visible to the tensor core (async proxy); S_t reads and W stores done
-      ptx::fence_proxy_async_smem();
+      // P_t in TMEM for the tensor core; S_t reads and W stores done
       tc::fence_before_sync();
       ptx::mbar_arrive(&p_full[g]);
       if (lane == 0) TC_MARK(warp, t, 5);
