@@ -105,12 +105,16 @@ __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& 
   y1 = __int_as_float(__float_as_int(q1) + (__float_as_int(r1) << 23));
 }
 
+#ifndef ELSA_TC_STAGES
+#define ELSA_TC_STAGES 4  // K/V ring depth (measured: 2: 697, 3: 827, 4: 845, 5: 845 TFLOP/s at 16K)
+#endif
+
 // anchor hysteresis of the deferred rescale (log2 units): P <= 2^8
 constexpr float kRescaleLog2 = 8.f;
 
 template <int GROUPS>
 struct TcTraits {
-  static constexpr int TQ = 128, TK = 128, D = 64, STAGES = 3;
+  static constexpr int TQ = 128, TK = 128, D = 64, STAGES = ELSA_TC_STAGES;
   static constexpr int ROWS = GROUPS * TQ;                   // query rows per CTA
   static constexpr int ROW_BYTES = D * 2;                    // 128 B per 16-bit row
   static constexpr int Q_BYTES = TQ * ROW_BYTES;             // 16 KB per group
