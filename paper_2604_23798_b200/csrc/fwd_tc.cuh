@@ -269,8 +269,9 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     // Each barrier is only ever tested for its next phase, which cannot
     // have been overtaken (every phase needs an MMA issued here first), and
     // with test_wait: a try_wait could park the warp on one group's barrier
-    // while the other group's P is ready. (Probing all barriers at once with
-    // one ballot, PV before S, measured slower: 700 vs 769 TFLOP/s at 16K.)
+    // while the other group's P is ready. (Measured slower: probing all
+    // barriers at once, one lane per barrier + ballot, 700 vs 769 TFLOP/s;
+    // lane 0 probing all barriers then one broadcast, 631 vs 834.)
     ptx::mbar_wait(qbar, 0);
     int ns[GROUPS], npv[GROUPS];  // next S tile / next P V tile per group
     for (int g = 0; g < GROUPS; ++g) ns[g] = npv[g] = 0;
