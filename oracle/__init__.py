@@ -37,6 +37,7 @@ from .attention import (  # noqa: F401
     U32,
     bound_threshold,
     naive_attention,
+    naive_attention_rows_fp64,
     partial_state_fp64,
     row_err_conditioned,
     row_rel_err,

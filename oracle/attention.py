@@ -63,6 +63,24 @@ def naive_attention(Q, K, V, scale=None, dtype=np.float64, return_p=False):
     return (Y, P) if return_p else Y
 
 
+def naive_attention_rows_fp64(Q, K, V, scale=None, rows_per_chunk=1024):
+    """FP64 naive attention (oracles.py:74-104 arithmetic) over query-row
+    chunks, so every row of a long sequence can be checked without an n x n
+    matrix in memory at once."""
+    Q, K, V = (np.asarray(x, dtype=np.float64) for x in (Q, K, V))
+    b, h, n_q, d = Q.shape
+    sc = _scale(d) if scale is None else float(scale)
+    Y = np.empty((b, h, n_q, V.shape[3]))
+    for bi in range(b):
+        for hi in range(h):
+            for r0 in range(0, n_q, rows_per_chunk):
+                s = (Q[bi, hi, r0:r0 + rows_per_chunk] @ K[bi, hi].T) * sc
+                s -= s.max(axis=1, keepdims=True)
+                np.exp(s, out=s)
+                Y[bi, hi, r0:r0 + rows_per_chunk] = (s @ V[bi, hi]) / s.sum(axis=1, keepdims=True)
+    return Y
+
+
 def vectorized_probs(Q, K, scale=None, dtype=np.float32):
     """Probability matrix of the batched pipeline (oracles.py:107-122)."""
     dt = np.dtype(dtype)

@@ -197,6 +197,18 @@ def test_leading_dims_and_out_argument():
     assert torch.equal(out[:, 0], y)
 
 
+# ------------------------------------------------- the reference's acceptance C4
+@pytest.mark.parametrize("n", [1024, 4096, 16384])
+def test_reference_acceptance_c4_all_rows(n):
+    # test_acceptance.py:161-182 (SPEC.md C4): seed 11, regular, d = 16,
+    # d_v = 8, FP32 — EVERY row within u * L(n, 128) * 8 of FP64
+    Q, K, V = oracle.generate(11, "regular", b=1, h=1, n=n, d=16, d_v=8, dtype=np.float32)
+    y = run(Q, K, V)
+    ref = oracle.naive_attention_rows_fp64(Q, K, V)
+    err = assert_bound(y, ref, n, f"C4 n={n}")
+    assert err.shape == (1, 1, n)
+
+
 # ---------------------------------------------------------------- determinism & splits
 def test_bitwise_deterministic_and_split_independent_within_bound():
     Q, K, V = oracle.generate(107, "regular", b=1, h=4, n=2048, d=64, d_v=64, dtype=np.float32)
