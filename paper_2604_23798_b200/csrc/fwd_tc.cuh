@@ -105,6 +105,11 @@ __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& 
   y1 = __int_as_float(__float_as_int(q1) + (__float_as_int(r1) << 23));
 }
 
+#ifndef ELSA_TC_SELF_ISSUE
+#define ELSA_TC_SELF_ISSUE 0  // each softmax warpgroup issues its own MMAs (measured: 506 vs 835 TFLOP/s at 16K — issuing blocks the softmax warp)
+#endif
+constexpr bool kTcSelfIssue = ELSA_TC_SELF_ISSUE != 0;
+
 #ifndef ELSA_TC_STAGES
 #define ELSA_TC_STAGES 4  // K/V ring depth (measured: 2: 697, 3: 827, 4: 845, 5: 845 TFLOP/s at 16K)
 #endif
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     ptx::mbar_init(qbar, 1);
     for (int s = 0; s < T::STAGES; ++s) {
       ptx::mbar_init(&kv_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], 1);
+      ptx::mbar_init(&kv_empty[s], kTcSelfIssue ? GROUPS : 1);
     }
     for (int g = 0; g < GROUPS; ++g) {
       ptx::mbar_init(&s_full[g], 1);
@@ -201,6 +206,40 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
   constexpr int kFmt = kBF16 ? 1 : 0;
   constexpr uint32_t kIdescS = tc::instr_desc_f16(kFmt, false, false, 128, 128);
   constexpr uint32_t kIdescO = tc::instr_desc_f16(kFmt, false, true, 128, 64);
+
+  // MMA issue for group g (warp-uniform; the elected `leader` lane issues)
+  auto issue_s = [&](int g, int t, bool leader) {  // S_g(t) = Q_g K_t^T
+    const int s = t % T::STAGES;
+    const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q + g * T::Q_BYTES);
+    const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K + s * T::K_BYTES);
+    const uint32_t d = tmem + T::S_COL + g * 128;
+#pragma unroll
+    for (int kk = 0; kk < T::D / 16; ++kk) {  // K-steps of 16 elements = 32 B
+      const uint64_t a = tc::smem_desc_sw128(q_addr + kk * 32, 16, 1024);
+      const uint64_t bd = tc::smem_desc_sw128(k_addr + kk * 32, 16, 1024);
+      if (leader) tc::mma_f16_ss(d, a, bd, kIdescS, kk > 0);
+    }
+    if (leader) tc::commit(&s_full[g]);
+    __syncwarp();
+  };
+  auto issue_o = [&](int g, int t, bool leader) {  // W_g (+)= P_g(t) V_t, P from TMEM
+    const int s = t % T::STAGES;
+    const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V + s * T::V_BYTES);
+    const uint32_t d = tmem + T::O_COL + g * 64;
+    const uint32_t pa = tmem + T::P_COL + g * 64;
+#pragma unroll
+    for (int kk = 0; kk < T::TK / 16; ++kk) {
+      // V: MN-major (rows = keys, 128 B each); 16 keys per step = 2 swizzle atoms
+      const uint64_t bd = tc::smem_desc_sw128(v_addr + kk * 2048, 16, 1024);
+      if (leader) tc::mma_f16_ts(d, pa + kk * 8, bd, kIdescO, (t > 0 || kk > 0) ? 1u : 0u);
+    }
+    if (leader) tc::commit(&o_full[g]);
+    __syncwarp();
+  };
+  // lane 0's view of a barrier phase, broadcast so the schedule stays uniform
+  auto ready = [&](uint64_t* bar, uint32_t parity) {
+    return __shfl_sync(0xffffffffu, ptx::mbar_test(bar, parity) ? 1 : 0, 0) != 0;
+  };
 
   // setmaxnreg inside each role's branch so the softmax code is dominated by
   // the .inc (ptxas then allocates up to SOFTMAX_REGS there)
@@ -224,45 +263,13 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
         ptx::tma_load_4d(smem + T::OFF_V + s * T::V_BYTES, &tmV, &kv_full[s], 0, t * T::TK, h, b);
       }
     }
-  } else if (warp == T::MMA_WARP) {
+  } else if (warp == T::MMA_WARP && !kTcSelfIssue) {
     // ---------------- MMA issuer ----------------
     // The whole warp runs the (warp-uniform) schedule so the descriptors stay
     // in uniform registers; one elected lane issues each tcgen05.mma / commit.
     // (A lane-0-only loop paid R2UR round trips per descriptor and measured
     // ~1300 clocks from a group's barrier to the matching issue.)
     const bool leader = tc::elect_one();
-    auto issue_s = [&](int g, int t) {  // S_g(t) = Q_g K_t^T
-      const int s = t % T::STAGES;
-      const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q + g * T::Q_BYTES);
-      const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K + s * T::K_BYTES);
-      const uint32_t d = tmem + T::S_COL + g * 128;
-#pragma unroll
-      for (int kk = 0; kk < T::D / 16; ++kk) {  // K-steps of 16 elements = 32 B
-        const uint64_t a = tc::smem_desc_sw128(q_addr + kk * 32, 16, 1024);
-        const uint64_t bd = tc::smem_desc_sw128(k_addr + kk * 32, 16, 1024);
-        if (leader) tc::mma_f16_ss(d, a, bd, kIdescS, kk > 0);
-      }
-      if (leader) tc::commit(&s_full[g]);
-      __syncwarp();
-    };
-    auto issue_o = [&](int g, int t) {  // W_g (+)= P_g(t) V_t, P from TMEM
-      const int s = t % T::STAGES;
-      const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V + s * T::V_BYTES);
-      const uint32_t d = tmem + T::O_COL + g * 64;
-      const uint32_t pa = tmem + T::P_COL + g * 64;
-#pragma unroll
-      for (int kk = 0; kk < T::TK / 16; ++kk) {
-        // V: MN-major (rows = keys, 128 B each); 16 keys per step = 2 swizzle atoms
-        const uint64_t bd = tc::smem_desc_sw128(v_addr + kk * 2048, 16, 1024);
-        if (leader) tc::mma_f16_ts(d, pa + kk * 8, bd, kIdescO, (t > 0 || kk > 0) ? 1u : 0u);
-      }
-      if (leader) tc::commit(&o_full[g]);
-      __syncwarp();
-    };
-    // lane 0's view of a barrier phase, broadcast so the schedule stays uniform
-    auto ready = [&](uint64_t* bar, uint32_t parity) {
-      return __shfl_sync(0xffffffffu, ptx::mbar_test(bar, parity) ? 1 : 0, 0) != 0;
-    };
     // Event loop over both groups: S_g(t+1) is issued as soon as group g
     // has pulled S_g(t) into registers (s_free) — it overlaps the group's own
     // exponentials — and P_g(t) V_t as soon as P_g(t) is written (p_full).
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
         if (u < ns[g] && ready(&p_full[g], u & 1)) {  // P V first: on the softmax's path
           tc::fence_after_sync();
           if (lane == 0) TC_MARK(8 + g, u, 1);
-          issue_o(g, u);
+          issue_o(g, u, leader);
           npv[g] = u + 1;
           int done = npv[0];
 #pragma unroll
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
             ready(&kv_full[t % T::STAGES], (t / T::STAGES) & 1)) {
           tc::fence_after_sync();
           if (lane == 0) TC_MARK(8 + g, t, 0);
-          issue_s(g, t);
+          issue_s(g, t, leader);
           ns[g] = t + 1;
         }
       }
@@ -317,6 +324,19 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     float m_run = -CUDART_INF_F;        // log2-domain anchor
     float l_run = 0.f;
     const uint32_t p_tm = tmem + lane_base + T::P_COL + g * 64;
+    // self-issue: warp 0 of the group issues the group's MMAs after a
+    // group-wide named barrier (id 1 + g) instead of signalling the MMA warp
+    const bool issuer = kTcSelfIssue && (warp & 3) == 0;
+    const bool leader = issuer && tc::elect_one();
+    auto group_sync = [&]() {
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+    };
+    if (issuer && ntiles > 0) {
+      ptx::mbar_wait(qbar, 0);
+      ptx::mbar_wait(&kv_full[0], 0);
+      tc::fence_after_sync();
+      issue_s(g, 0, leader);
+    }
 
     for (int t = 0; t < ntiles; ++t) {
       if (lane == 0) TC_MARK(warp, t, 0);
@@ -334,7 +354,16 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       tc::tmem_wait_ld();
       // S_g(t) is in registers: the tensor core may overwrite it with S_g(t+1)
       tc::fence_before_sync();
-      ptx::mbar_arrive(&s_free[g]);
+      if constexpr (kTcSelfIssue) {
+        group_sync();
+        if (issuer && t + 1 < ntiles) {
+          ptx::mbar_wait(&kv_full[(t + 1) % T::STAGES], ((t + 1) / T::STAGES) & 1);
+          tc::fence_after_sync();
+          issue_s(g, t + 1, leader);
+        }
+      } else {
+        ptx::mbar_arrive(&s_free[g]);
+      }
       if (lane == 0) TC_MARK(warp, t, 2);
       const int kv_hi = p.n_kv - t * T::TK;  // valid keys in this tile
       if (kv_hi < T::TK) {                   // tail tile (warp-uniform): mask past n_kv
@@ -442,7 +471,17 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       l_run = fmaf(l_run, corr, psum);
       // P_t in TMEM for the tensor core; S_t reads and W stores done
       tc::fence_before_sync();
-      ptx::mbar_arrive(&p_full[g]);
+      if constexpr (kTcSelfIssue) {
+        group_sync();
+        if (issuer) {
+          tc::fence_after_sync();
+          issue_o(g, t, leader);
+          if (leader) tc::commit(&kv_empty[t % T::STAGES]);
+          __syncwarp();
+        }
+      } else {
+        ptx::mbar_arrive(&p_full[g]);
+      }
       if (lane == 0) TC_MARK(warp, t, 5);
     }
     // ---- epilogue: Y = W / S (engine.py:375-382) in the input's 16-bit format ----
