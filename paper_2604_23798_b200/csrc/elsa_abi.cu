@@ -743,7 +743,16 @@ int elsa_fwd_f32_host(const float* q, const float* k, const float* v, float* y,
     launches += t_last_launches;
     t_last_launches = 0;
     e = cudaEventRecord(hp->ev_comp[g], cs);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(hp->out, hp->ev_comp[g], 0);
+    if (e != cudaSuccess) return fail(e, "host pipeline record");
+  }
+  // D2H copies after every H2D and launch is enqueued: with pageable host
+  // buffers each copy call blocks the host until its data moved, so the
+  // later groups' staging and kernels must already be in flight
+  for (int g = 0; g < L.groups; ++g) {
+    const int64_t bh0 = int64_t(g) * L.hpg;
+    const int64_t cnt = BH - bh0 < L.hpg ? BH - bh0 : L.hpg;
+    const size_t yo = size_t(bh0 * nq * dvw);
+    e = cudaStreamWaitEvent(hp->out, hp->ev_comp[g], 0);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(y + yo, dy + yo, size_t(cnt * nq * dvw) * 4, cudaMemcpyDeviceToHost,
                           hp->out);
