@@ -70,12 +70,18 @@ __device__ __forceinline__ void scan_combine(float* base, int pitch, int dv, int
   }
 }
 
+// kSmem: the row's padded state array lives in shared memory (one slice per
+// warp) instead of the global workspace — the sweeps then never leave the SM
+// (used while K_pad * (2 + dv) * 4 B per warp fits).
+template <bool kSmem>
 __global__ void __launch_bounds__(256) block_scan_f32_kernel(const BlockScanParams p) {
+  extern __shared__ __align__(16) float scan_smem[];
   const int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= p.rows) return;
   const int pitch = 2 + p.dv;
-  float* base = p.ws + row * int64_t(p.K_pad) * pitch;
+  float* base = kSmem ? scan_smem + (threadIdx.x >> 5) * p.K_pad * pitch
+                      : p.ws + row * int64_t(p.K_pad) * pitch;
 
   // load + identity padding
   for (int i = 0; i < p.K_pad; ++i) {

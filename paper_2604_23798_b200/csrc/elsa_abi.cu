@@ -1027,7 +1027,25 @@ int elsa_block_scan_f32(const float* m, const float* S, const float* W, int64_t 
   constexpr int kWarps = 8;
   const int64_t blocks = ceil_div(rows, kWarps);
   if (blocks >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
-  block_scan_f32_kernel<<<unsigned(blocks), kWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(bp);
+  // per-warp slice of the padded array in shared memory when it fits (the
+  // global workspace is still required by the ABI and used beyond that)
+  const size_t smem = size_t(kWarps) * size_t(bp.K_pad) * size_t(2 + dv) * sizeof(float);
+  if (smem <= 48 * 1024) {  // larger slices cost more occupancy than they save (measured K = 32)
+    static bool attr_set[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < kMaxDevices && !attr_set[dev]) {
+      const cudaError_t e = cudaFuncSetAttribute(
+          block_scan_f32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(block scan)");
+      attr_set[dev] = true;
+    }
+    block_scan_f32_kernel<true><<<unsigned(blocks), kWarps * 32, smem,
+                                  static_cast<cudaStream_t>(stream)>>>(bp);
+  } else {
+    block_scan_f32_kernel<false><<<unsigned(blocks), kWarps * 32, 0,
+                                   static_cast<cudaStream_t>(stream)>>>(bp);
+  }
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "block scan launch");
   ++t_last_launches;
   return ELSA_OK;
