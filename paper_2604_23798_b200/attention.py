@@ -279,7 +279,9 @@ def attention_from_host(query, key, value, scale=None, *, out=None, kv_splits=0,
     B, H, n_q, _ = q.shape
     dv = v.shape[-1]
     if out is None:
-        y = torch.empty((B, H, n_q, dv), dtype=torch.float32, pin_memory=q.is_pinned())
+        # pageable: a fresh page-locked allocation per call would cost more than
+        # the copy it speeds up (pass a pinned `out` to reuse one)
+        y = torch.empty((B, H, n_q, dv), dtype=torch.float32)
     else:
         y = out
         if tuple(y.shape) != (B, H, n_q, dv) or y.dtype != torch.float32 or y.is_cuda \
