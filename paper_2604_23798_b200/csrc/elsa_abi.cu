@@ -714,8 +714,11 @@ int elsa_fwd_f32_host(const float* q, const float* k, const float* v, float* y,
   int launches = 0;
   auto fail = [&](cudaError_t e, const char* where) { return cuda_fail(e, where); };
 
+  // after the caller's prior work and after every earlier host-pipeline call
+  // on this device (they share these streams and usually the workspace)
   cudaError_t e = cudaEventRecord(hp->start, caller);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(hp->in, hp->start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(hp->in, hp->done, 0);
   if (e != cudaSuccess) return fail(e, "host pipeline start");
   for (int g = 0; g < L.groups; ++g) {
     const int64_t bh0 = int64_t(g) * L.hpg;
