@@ -462,6 +462,31 @@ def main():
                           "B": B, "H": H, "n": n, "ms": tms, "tflops": fl / (tms * 1e-3) / 1e12})
         except Exception as exc:  # noqa: BLE001
             sweep.append({"comparator": "torch sdpa fp32", "error": str(exc)[:200]})
+        # the FP16/BF16 variant (K5, tcgen05) on the same problem, for comparison
+        # (BASELINE configs[4]); flops 4*B*H*n^2*64, same as the FP32 count
+        for dt, nm in ((torch.bfloat16, "bf16"), (torch.float16, "fp16")):
+            try:
+                q16, k16, v16 = q.to(dt), k.to(dt), v.to(dt)
+                row = {"variant": f"elsa {nm} (tcgen05)", "B": B, "H": H, "n": n}
+                for label, fn in (("elsa", lambda: elsa.scaled_dot_product_attention(q16, k16, v16)),
+                                  ("torch", lambda: torch.nn.functional.scaled_dot_product_attention(
+                                      q16, k16, v16))):
+                    for _ in range(2):
+                        fn()
+                    s0 = torch.cuda.Event(enable_timing=True)
+                    s1 = torch.cuda.Event(enable_timing=True)
+                    s0.record(stream)
+                    for _ in range(5):
+                        fn()
+                    s1.record(stream)
+                    torch.cuda.synchronize()
+                    tms = s0.elapsed_time(s1) / 5
+                    row[f"{label}_ms"] = tms
+                    row[f"{label}_tflops"] = fl / (tms * 1e-3) / 1e12
+                sweep.append(row)
+                del q16, k16, v16
+            except Exception as exc:  # noqa: BLE001
+                sweep.append({"variant": f"elsa {nm}", "error": str(exc)[:200]})
 
     # ---- CPU baseline: the reference's algorithm on the host cores (rank 0, N=1) ----
     cpu = None
