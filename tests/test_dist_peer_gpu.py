@@ -26,6 +26,7 @@ DEV = torch.device("cuda", 0)
 
 @pytest.fixture(scope="module")
 def pg():
+    created = False
     if not dist.is_initialized():
         with socket.socket() as s:
             s.bind(("127.0.0.1", 0))
@@ -34,7 +35,12 @@ def pg():
         os.environ["MASTER_PORT"] = str(port)
         torch.cuda.set_device(DEV)
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+        created = True
     yield dist.group.WORLD
+    if created:
+        torch.cuda.synchronize()
+        edist._PEER_BUFS.clear()
+        dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("B,H,n,chunks", [(1, 4, 1000, 8), (2, 3, 513, 4), (1, 2, 4096, 8)])
