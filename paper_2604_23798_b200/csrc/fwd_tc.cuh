@@ -279,7 +279,8 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     // while the other group's P is ready. (Measured slower: probing all
     // barriers at once, one lane per barrier + ballot, 700 vs 769 TFLOP/s;
     // lane 0 probing all barriers then one broadcast, 631 vs 834; S and P V
-    // issued by two separate warps, 815 vs 835.)
+    // issued by two separate warps, 815 vs 835; one issuing warp per group,
+    // 730 vs 837 — a single issuer is best.)
     ptx::mbar_wait(qbar, 0);
     int ns[GROUPS], npv[GROUPS];  // next S tile / next P V tile per group
     for (int g = 0; g < GROUPS; ++g) ns[g] = npv[g] = 0;
