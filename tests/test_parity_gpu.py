@@ -381,3 +381,23 @@ def test_c4_64k_single_gpu_and_kv_chunked_path():
     y2 = edist.kv_sharded_attention(q, k, v, 0, n, chunks=8)
     _sampled_check(q, k, v, n, [3], 6, y2, "C4 kv-chunked")
     assert torch.allclose(y, y2, rtol=1e-4, atol=1e-5)
+
+
+# ---------------------------------------------------------------- unusual geometries
+@pytest.mark.parametrize("B,H,n_q,n_kv", [
+    (64, 16, 64, 64),      # many tiny heads: one tile each, 1024 CTAs
+    (1, 2, 1, 131072),     # decode-like: one query row, a long key range (split chains)
+    (2, 3, 777, 1),        # one key: y = v exactly
+    (1, 1, 5000, 333),     # ragged query tiles over a short key range
+])
+def test_unusual_geometries(B, H, n_q, n_kv):
+    rng = np.random.default_rng(B * 1000 + n_kv)
+    Q = rng.standard_normal((B, H, n_q, 64)).astype(np.float32)
+    K = rng.standard_normal((B, H, n_kv, 64)).astype(np.float32)
+    V = rng.standard_normal((B, H, n_kv, 64)).astype(np.float32)
+    y = run(Q, K, V)
+    if n_kv == 1:
+        assert np.array_equal(y, np.broadcast_to(V, y.shape))
+        return
+    ref = oracle.naive_attention_rows_fp64(Q, K, V)
+    assert_bound(y, ref, n_kv, f"{B}x{H}x{n_q}x{n_kv}")
