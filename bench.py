@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--dist-path", action="store_true",
                     help="run the KV-sharded multi-GPU code path even at N = 1 (a world-size-1 "
                          "NCCL group; checks the N > 1 path on a single GPU)")
+    ap.add_argument("--shard", choices=["kv", "q"], default="kv",
+                    help="N > 1: KV-sharded (Proposition 1, the product) or query-sharded "
+                         "(no exchange; SURVEY 8e's control experiment)")
     ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
                     help="N > 1: state exchange + merge over symmetric peer memory (one "
                          "kernel) or NCCL all_to_all + merge kernel")
@@ -262,12 +265,15 @@ def main():
             y = elsa.scaled_dot_product_attention(q, k, v)
             launches[0] += elsa.last_launch_count()
             return y
-        r = edist.kv_sharded_attention(q, k_loc, v_loc, off, n, chunks=chunks, gather=False,
-                                       exchange=exchange[0])
+        if args.shard == "q":
+            r = edist.query_sharded_attention(q, k, v)
+        else:
+            r = edist.kv_sharded_attention(q, k_loc, v_loc, off, n, chunks=chunks, gather=False,
+                                           exchange=exchange[0])
         launches[0] += 2 * (chunks // world) + 1
         return r
 
-    if sharded and exchange[0] == "peer":
+    if sharded and args.shard == "kv" and exchange[0] == "peer":
         # the symmetric-memory rendezvous needs peer access between every pair
         # of GPUs; if this node cannot provide it, measure the NCCL exchange
         try:
@@ -319,17 +325,21 @@ def main():
     if not args.no_e2e and sharded:
         # each rank: H2D of Q and its K/V shard, the KV-sharded forward, D2H of
         # its Y row slice (the ranks' slices together are the whole Y)
+        k_src, v_src = (k, v) if args.shard == "q" else (k_loc, v_loc)
         hq = q.cpu().pin_memory()
-        hk, hv = k_loc.cpu().pin_memory(), v_loc.cpu().pin_memory()
-        dq, dk, dv_ = torch.empty_like(q), torch.empty_like(k_loc), torch.empty_like(v_loc)
+        hk, hv = k_src.cpu().pin_memory(), v_src.cpu().pin_memory()
+        dq, dk, dv_ = torch.empty_like(q), torch.empty_like(k_src), torch.empty_like(v_src)
         hy = [None]
 
         def e2e_step_dist():
             dq.copy_(hq, non_blocking=True)
             dk.copy_(hk, non_blocking=True)
             dv_.copy_(hv, non_blocking=True)
-            _, yr = edist.kv_sharded_attention(dq, dk, dv_, off, n, chunks=chunks, gather=False,
-                                               exchange=exchange[0])
+            if args.shard == "q":
+                _, yr = edist.query_sharded_attention(dq, dk, dv_)
+            else:
+                _, yr = edist.kv_sharded_attention(dq, dk, dv_, off, n, chunks=chunks,
+                                                   gather=False, exchange=exchange[0])
             if hy[0] is None:
                 hy[0] = torch.empty(yr.shape, dtype=yr.dtype).pin_memory()
             hy[0].copy_(yr, non_blocking=True)
@@ -350,7 +360,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
         e2e = {"value": fl / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": (q.numel() + k_loc.numel() + v_loc.numel()) * 4 * world,
+               "h2d_bytes_per_step": (q.numel() + k_src.numel() + v_src.numel()) * 4 * world,
                "d2h_bytes_per_step": hy[0].numel() * 4 * world, "steps": steps_e2e,
                "api": "paper_2604_23798_b200.dist.kv_sharded_attention per rank, pinned host "
                       "buffers (bytes summed over ranks; max-over-ranks time)"}
@@ -510,7 +520,8 @@ def main():
                        "l2": "inputs 3x%.0f MB > 126 MB L2; sweep flushes L2 (256 MB write) "
                              "between timed iterations" % (q.numel() * 4 / 1e6),
                        "parallelism": f"kv-shard{world}" if sharded else "single GPU",
-                       "exchange": exchange[0] if sharded else None},
+                       "exchange": (exchange[0] if args.shard == "kv" else "none (query-sharded)")
+                                   if sharded else None},
             "e2e": e2e, "gpu_launches": timed_launches, "clocks": clock_info,
             "roofline": roofline, "cpu_baseline": cpu, "sweep": sweep,
         }

@@ -43,7 +43,7 @@ import torch.distributed as dist
 from .errors import ShapeError
 
 __all__ = ["chunk_bounds", "owned_chunks", "row_slices", "kv_sharded_attention",
-           "shard_kv", "DEFAULT_CHUNKS"]
+           "query_sharded_attention", "shard_kv", "DEFAULT_CHUNKS"]
 
 DEFAULT_CHUNKS = 8
 
@@ -221,4 +221,49 @@ def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
     outs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(outs, pad, group=group)
     y = torch.cat([o[: hi - lo] for o, (lo, hi) in zip(outs, slices)])
+    return y.reshape(B, H, n_q, dv)
+
+
+def query_sharded_attention(q, k, v, group=None, gather=False):
+    """The control experiment of SURVEY §8e: rank r computes the query rows of
+    its slice (flattened (b, h, q) order, the same slices as the KV-sharded
+    path) against ALL keys — no exchange, no merge. Returns ``(row_begin,
+    Y_rows)``, or the full Y with ``gather``."""
+    from .attention import scaled_dot_product_attention
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    B, H, n_q, d = q.shape
+    dv = v.shape[-1]
+    rows = B * H * n_q
+    slices = row_slices(rows, world)
+    lo, hi = slices[rank]
+    # the slice = [partial head] + whole heads (one launch) + [partial head]
+    qf, kf, vf = (t.reshape(B * H, 1, t.shape[2], t.shape[3]) for t in (q, k, v))
+    out = torch.empty((hi - lo, dv), device=q.device, dtype=torch.float32)
+    r = lo
+    while r < hi:
+        bh, q0 = divmod(r, n_q)
+        if q0 == 0 and hi - r >= n_q:  # a run of whole heads
+            nh = (hi - r) // n_q
+            y = scaled_dot_product_attention(qf[bh:bh + nh].transpose(0, 1),
+                                             kf[bh:bh + nh].transpose(0, 1),
+                                             vf[bh:bh + nh].transpose(0, 1))
+            out[r - lo: r - lo + nh * n_q] = y.reshape(nh * n_q, dv)
+            r += nh * n_q
+        else:
+            q1 = min(n_q, q0 + (hi - r))
+            y = scaled_dot_product_attention(qf[bh:bh + 1, :, q0:q1], kf[bh:bh + 1], vf[bh:bh + 1])
+            out[r - lo: r - lo + (q1 - q0)] = y.reshape(q1 - q0, dv)
+            r += q1 - q0
+    if not gather:
+        return lo, out
+    if world == 1:
+        return out.reshape(B, H, n_q, dv)
+    maxr = max(b_ - a_ for a_, b_ in slices)
+    pad = torch.zeros((maxr, dv), dtype=torch.float32, device=q.device)
+    pad[: out.shape[0]] = out
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    y = torch.cat([o[: b_ - a_] for o, (a_, b_) in zip(outs, slices)])
     return y.reshape(B, H, n_q, dv)

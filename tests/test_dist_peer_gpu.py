@@ -58,3 +58,12 @@ def test_peer_exchange_matches_nccl_and_oracle(pg, B, H, n, chunks):
     lo, rows = edist.kv_sharded_attention(q, kl, vl, off, n, chunks=chunks, exchange="peer",
                                           gather=False)
     assert lo == 0 and torch.equal(rows, y_peer.reshape(-1, 64))
+
+
+@pytest.mark.parametrize("B,H,n", [(1, 4, 1000), (2, 3, 513)])
+def test_query_sharded_control_matches_direct(pg, B, H, n):
+    g = torch.Generator(device=DEV)
+    g.manual_seed(B * H + n)
+    q, k, v = (torch.randn(B, H, n, 64, device=DEV, generator=g) for _ in range(3))
+    y = edist.query_sharded_attention(q, k, v, gather=True)
+    assert torch.equal(y, elsa.scaled_dot_product_attention(q, k, v))
