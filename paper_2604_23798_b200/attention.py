@@ -39,6 +39,12 @@ __all__ = [
 ]
 
 
+
+# Widest heads the FP32 kernels take (elsa_abi.cu kMaxD / kMaxDv): Q/K up to
+# 128 floats wide; V of any width up to 4096 as 64-column slices.
+MAX_D = 128
+MAX_DV = 4096
+
 def _stream_ptr(device):
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
@@ -102,8 +108,9 @@ def _shape(q, k, v, y=None):
         raise ShapeError(f"value length {n_v} != key length {n_kv}")
     if n_kv < 1:
         raise ShapeError("key/value length must be >= 1")
-    if d > 64 or dv > 64:
-        raise ShapeError(f"head dims d={d}, dv={dv}: libelsa supports d, dv <= 64")
+    if d > MAX_D or dv > MAX_DV:
+        raise ShapeError(f"head dims d={d}, dv={dv}: libelsa supports d <= {MAX_D}, "
+                         f"dv <= {MAX_DV}")
     s = _lib.ElsaShape()
     s.B, s.H, s.n_q, s.n_kv, s.d, s.dv = B, H, n_q, n_kv, d, dv
     for dst, t in ((s.q_stride, q), (s.k_stride, k), (s.v_stride, v)):

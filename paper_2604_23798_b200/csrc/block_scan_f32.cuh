@@ -16,7 +16,7 @@
 // bitwise equal; elsewhere they differ only by the exp rounding (CUDA expf vs
 // numpy's SIMD exp, both within a few ulp).
 //
-// One warp per row: the lanes own W columns (lane, lane + 32); m and S are
+// One warp per row: lane c owns W columns c, c + 32, ...; m and S are
 // evaluated redundantly by every lane (broadcast loads) and stored by lane 0.
 // The padded array lives in a global workspace [rows][K_pad][2 + dv].
 #pragma once
@@ -58,12 +58,9 @@ __device__ __forceinline__ void scan_combine(float* base, int pitch, int dv, int
   float* wa = base + int64_t(a) * pitch + 2;
   float* wb = base + int64_t(b) * pitch + 2;
   float* wd = base + int64_t(dst) * pitch + 2;
-  float r0 = 0.f, r1 = 0.f;
-  if (lane < dv) r0 = __fadd_rn(__fmul_rn(wa[lane], fa), __fmul_rn(wb[lane], fb));
-  if (lane + 32 < dv) r1 = __fadd_rn(__fmul_rn(wa[lane + 32], fa), __fmul_rn(wb[lane + 32], fb));
+  // each lane reads and writes only its own columns, so in-place is safe
+  for (int c = lane; c < dv; c += 32) wd[c] = __fadd_rn(__fmul_rn(wa[c], fa), __fmul_rn(wb[c], fb));
   __syncwarp();
-  if (lane < dv) wd[lane] = r0;
-  if (lane + 32 < dv) wd[lane + 32] = r1;
   if (lane == 0) {
     base[int64_t(dst) * pitch] = mm;
     base[int64_t(dst) * pitch + 1] = __fadd_rn(__fmul_rn(Sa, fa), __fmul_rn(Sb, fb));
@@ -138,24 +135,12 @@ __global__ void __launch_bounds__(256) block_scan_f32_kernel(const BlockScanPara
       const float mo = sl[0], So = sl[1], mp = sr[0], Sp = sr[1];
       const float mm = fmaxf(mp, mo);
       const float fp = scan_factor(mp, mm), fo = scan_factor(mo, mm);
-      float wo0 = 0.f, wo1 = 0.f, wp0 = 0.f, wp1 = 0.f;
-      if (lane < p.dv) {
-        wo0 = sl[2 + lane];
-        wp0 = sr[2 + lane];
-      }
-      if (lane + 32 < p.dv) {
-        wo1 = sl[2 + lane + 32];
-        wp1 = sr[2 + lane + 32];
-      }
-      __syncwarp();
-      // left <- prefix; right <- prefix (+) old left
-      if (lane < p.dv) {
-        sl[2 + lane] = wp0;
-        sr[2 + lane] = __fadd_rn(__fmul_rn(wp0, fp), __fmul_rn(wo0, fo));
-      }
-      if (lane + 32 < p.dv) {
-        sl[2 + lane + 32] = wp1;
-        sr[2 + lane + 32] = __fadd_rn(__fmul_rn(wp1, fp), __fmul_rn(wo1, fo));
+      __syncwarp();  // every lane has read the m / S words above
+      // left <- prefix; right <- prefix (+) old left (per lane, its own columns)
+      for (int c = lane; c < p.dv; c += 32) {
+        const float wo = sl[2 + c], wp = sr[2 + c];
+        sl[2 + c] = wp;
+        sr[2 + c] = __fadd_rn(__fmul_rn(wp, fp), __fmul_rn(wo, fo));
       }
       if (lane == 0) {
         sl[0] = mp;

@@ -107,8 +107,29 @@ int current_device_cache(DeviceCache** out) {
 //   w8r8 : 8 consumer warps x 16 rows (TQ = 128), 1 CTA / SM
 //   w8r16: 8 consumer warps x 32 rows (TQ = 256), 1 CTA / SM, 16 rows per
 //          lane (setmaxnreg register split with a producer warpgroup)
+//   w8r8d128: w8r8 with Q/K 128 floats wide (64 < d <= 128; Q^T and the K
+//          ring fill 200 KB, raw Q is staged in the K ring)
+//   w8r8v128, w8r8d128v128: 128 V columns per CTA (dv > 64): a 128-column
+//          W accumulator (setmaxnreg register split with a producer
+//          warpgroup); with d > 64 too, P^T goes through shared memory in
+//          two key halves so that everything fits 227 KB
+// dv wider than the configuration's V width runs as column slices (grid z),
+// each recomputing its tile's scores: m / S are identical across slices.
 // ---------------------------------------------------------------------------
-enum CfgId { kCfgW4R8 = 0, kCfgW8R16 = 1, kCfgW8R8 = 2, kCfgCount = 3, kCfgAuto = -1 };
+enum CfgId {
+  kCfgW4R8 = 0,
+  kCfgW8R16 = 1,
+  kCfgW8R8 = 2,
+  kCfgCount = 3,  // the d <= 64 configurations the planner chooses from
+  kCfgW8R8D128 = 3,
+  kCfgW8R8V128 = 4,
+  kCfgW8R8D128V128 = 5,
+  kCfgAuto = -1
+};
+int cfg_dv(int cfg) { return cfg >= kCfgW8R8V128 ? 128 : 64; }
+constexpr int64_t kMaxD = 128;
+constexpr int64_t kMaxDv = 4096;
+int64_t dv_slices(int64_t dv) { return (dv + 63) / 64; }
 
 int forced_cfg() {
   static int cfg = [] {
@@ -136,6 +157,12 @@ CfgInfo cfg_info(int cfg) {
       return {256, 64, 1, 10.75, 7.6};
     case kCfgW8R8:
       return {128, 64, 1, 5.355, 4.1};
+    case kCfgW8R8D128:  // GEMM1 twice as long: ~1.5x the d = 64 tile
+      return {128, 64, 1, 8.03, 6.2};
+    case kCfgW8R8V128:  // GEMM2 twice as long
+      return {128, 64, 1, 8.03, 6.2};
+    case kCfgW8R8D128V128:
+      return {128, 64, 1, 10.7, 8.2};
     default:
       return {64, 64, 2, 2.711, 1.6};
   }
@@ -144,7 +171,7 @@ CfgInfo cfg_info(int cfg) {
 bool valid_shape(const elsa_shape* s) {
   if (!s) return false;
   if (s->B < 0 || s->H < 0 || s->n_q < 0 || s->n_kv < 1) return false;
-  if (s->d < 1 || s->d > 64 || s->dv < 1 || s->dv > 64) return false;
+  if (s->d < 1 || s->d > kMaxD || s->dv < 1 || s->dv > kMaxDv) return false;
   const int64_t lim = int64_t(1) << 31;
   if (s->B >= lim || s->H >= lim || s->n_q >= lim || s->n_kv >= lim) return false;
   if (s->B * s->H >= lim) return false;
@@ -167,7 +194,7 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // 4.0e-6 at 64K (bound 1.3e-5); 16384 measured 2.5e-5 (over).
 constexpr int64_t kMaxChainTiles = 1024;
 // Split workspace budget for auto planning (partial states are
-// (2 + 64) * 4 B per row per split): 4 GiB unless ELSA_MAX_WORKSPACE_MB says
+// (2 + 64 * dv slices) * 4 B per row per split): 4 GiB unless ELSA_MAX_WORKSPACE_MB says
 // otherwise. Explicit kv_splits requests are not capped.
 int64_t workspace_budget() {
   static const int64_t b = [] {
@@ -203,17 +230,22 @@ int64_t normalize_splits(int64_t s, int64_t tiles) {
 
 Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms) {
   const int64_t BH = sh->B * sh->H;
-  Plan best{kCfgW4R8, 1, BH > 0 ? BH : 1};
+  // head widths beyond 64 have one configuration each; d, dv <= 64 choose
+  const int wide = (sh->d > 64 ? 1 : 0) | (sh->dv > 64 ? 2 : 0);
+  const int only[4] = {-1, kCfgW8R8D128, kCfgW8R8V128, kCfgW8R8D128V128};
+  const int first = wide ? only[wide] : 0, last = wide ? only[wide] + 1 : int(kCfgCount);
+  Plan best{first, 1, BH > 0 ? BH : 1};
   double best_t = 1e300;
-  const int forced = forced_cfg();
-  const int64_t head_bytes = sh->n_q * (2 + 64) * 4;  // one split of one (b, h) head
-  for (int cfg = 0; cfg < kCfgCount; ++cfg) {
+  const int forced = wide ? int(kCfgAuto) : forced_cfg();
+  const int64_t slices = ceil_div(sh->dv, cfg_dv(first));
+  const int64_t head_bytes = sh->n_q * (2 + 64 * dv_slices(sh->dv)) * 4;  // one split of one (b, h) head
+  for (int cfg = first; cfg < last; ++cfg) {
     if (forced != kCfgAuto && cfg != forced) continue;
     const CfgInfo ci = cfg_info(cfg);
-    const int64_t ctas = ceil_div(sh->n_q, ci.tq) * BH;
+    const int64_t ctas = ceil_div(sh->n_q, ci.tq) * BH * slices;
     const int64_t tiles = ceil_div(kv_len, ci.tk);
     const int64_t rows = BH * sh->n_q;
-    if (ctas == 0 || tiles < 1) return Plan{forced == kCfgAuto ? int(kCfgW4R8) : forced, 1, 1};
+    if (ctas == 0 || tiles < 1) return Plan{forced == kCfgAuto ? first : forced, 1, 1};
     int64_t lo, hi;
     if (requested > 0) {
       lo = hi = normalize_splits(requested, tiles);
@@ -276,11 +308,11 @@ bool encode_map(CUtensorMap* map, const float* base, int64_t inner, int64_t rows
   return r == CUDA_SUCCESS;
 }
 
-template <int W, int TK, int ST, int R>
+template <int W, int TK, int ST, int R, int D = 64, int DV = 64>
 int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[3],
                    int64_t v_st[3], int splits, int64_t bh_count, int cfg_slot, DeviceCache* dc,
                    cudaStream_t stream) {
-  using T = FwdTraits<W, TK, ST, R>;
+  using T = FwdTraits<W, TK, ST, R, D, DV>;
   p.qtiles = int(ceil_div(s->n_q, T::TQ));
   const int64_t tiles = ceil_div(int64_t(p.kv_end) - p.kv_begin, TK);
   if (p.split_keys == 0) p.split_keys = int(ceil_div(tiles, splits) * TK);
@@ -296,7 +328,8 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
   static const bool force_generic = std::getenv("ELSA_FORCE_GENERIC_LOAD") != nullptr;
   if (force_generic) use_tma = false;
 
-  auto kern = use_tma ? fwd_f32_kernel<W, TK, ST, R, true> : fwd_f32_kernel<W, TK, ST, R, false>;
+  auto kern = use_tma ? fwd_f32_kernel<W, TK, ST, R, true, D, DV>
+                      : fwd_f32_kernel<W, TK, ST, R, false, D, DV>;
   const int slot = cfg_slot * 2 + (use_tma ? 1 : 0);
   if (!dc->attr[slot]) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -306,7 +339,7 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
   }
   const int64_t gx = int64_t(p.qtiles) * bh_count;
   if (gx >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
-  const dim3 grid{unsigned(gx), unsigned(splits), 1u};
+  const dim3 grid{unsigned(gx), unsigned(splits), unsigned(ceil_div(s->dv, DV))};
   kern<<<grid, T::THREADS, T::SMEM_BYTES, stream>>>(p, maps[0], maps[1], maps[2]);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "fwd launch");
   ++t_last_launches;
@@ -324,6 +357,15 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
     case kCfgW8R8:
       return launch_fwd_cfg<8, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8, dc,
                                          stream);
+    case kCfgW8R8D128:
+      return launch_fwd_cfg<8, 64, 2, 8, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
+                                              kCfgW8R8D128, dc, stream);
+    case kCfgW8R8V128:
+      return launch_fwd_cfg<8, 64, 2, 8, 64, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
+                                                  kCfgW8R8V128, dc, stream);
+    case kCfgW8R8D128V128:
+      return launch_fwd_cfg<8, 64, 2, 8, 128, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
+                                                   kCfgW8R8D128V128, dc, stream);
     default:
       return launch_fwd_cfg<4, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW4R8, dc,
                                          stream);
@@ -335,12 +377,13 @@ int launch_merge(MergeParams& mp, cudaStream_t stream) {
   constexpr int kWarps = 8;
   const int64_t blocks = ceil_div(mp.rows, kWarps);
   if (blocks >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
+  const dim3 grid{unsigned(blocks), unsigned(dv_slices(mp.dv)), 1u};
   auto kern = mp.parts <= 2    ? merge_f32_kernel<2>
               : mp.parts <= 4  ? merge_f32_kernel<4>
               : mp.parts <= 8  ? merge_f32_kernel<8>
               : mp.parts <= 16 ? merge_f32_kernel<16>
                                : merge_f32_kernel<32>;
-  kern<<<unsigned(blocks), kWarps * 32, 0, stream>>>(mp);
+  kern<<<grid, kWarps * 32, 0, stream>>>(mp);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "merge launch");
   ++t_last_launches;
   return ELSA_OK;
@@ -382,7 +425,7 @@ void fill_common(FwdParams& p, const float* q, const float* k, const float* v,
 size_t split_ws_bytes(const elsa_shape* s, const Plan& pl) {
   if (pl.splits <= 1) return 0;
   const size_t rows = size_t(pl.heads_per_batch) * size_t(s->n_q);
-  return size_t(pl.splits) * rows * (2 + 64) * sizeof(float);
+  return size_t(pl.splits) * rows * size_t(2 + 64 * dv_slices(s->dv)) * sizeof(float);
 }
 
 bool encode_map16(CUtensorMap* map, const void* base, int64_t rows, int64_t H, int64_t B,
@@ -427,9 +470,7 @@ int run_forward(const float* q, const float* k, const float* v, const elsa_shape
 
   const int64_t BH = shp->B * shp->H;
   const int64_t len = kv_end - kv_begin;
-  const Plan plan = len == 0        ? Plan{kCfgW4R8, 1, BH}
-                    : force_plan ? *force_plan
-                                 : plan_for(shp, len, kv_splits, dc->sms);
+  const Plan plan = force_plan ? *force_plan : plan_for(shp, len > 0 ? len : 1, kv_splits, dc->sms);
   const bool final_out = y != nullptr;
   FwdParams p;
   fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
@@ -472,7 +513,7 @@ int run_forward(const float* q, const float* k, const float* v, const elsa_shape
     p.pS = ws + int64_t(splits) * rows;
     p.pW = ws + int64_t(splits) * rows * 2;
     p.part_stride = rows;
-    p.pw_pitch = 64;
+    p.pw_pitch = int(64 * dv_slices(shp->dv));
     p.pw_vec = 1;
     if (int st = launch_fwd(p, shp, q_st, k_st, v_st, plan, cnt, dc, strm)) return st;
     MergeParams mp;
@@ -483,7 +524,7 @@ int run_forward(const float* q, const float* k, const float* v, const elsa_shape
     mp.parts = splits;
     mp.rows = rows;
     mp.dv = int(shp->dv);
-    mp.w_pitch = 64;
+    mp.w_pitch = int(64 * dv_slices(shp->dv));
     mp.part_stride = rows;
     mp.log2_domain = 1;
     mp.err = dc->err;
@@ -865,7 +906,7 @@ int elsa_merge_f32(const float* m, const float* S, const float* W, int parts, in
                    int dv, int64_t part_stride, int finalize, float* y, float* m_out,
                    float* S_out, float* W_out, void* stream) {
   t_last_launches = 0;
-  if (parts < 1 || parts > kMergeMaxParts || rows < 0 || dv < 1 || dv > 64) return ELSA_ERR_SHAPE;
+  if (parts < 1 || parts > kMergeMaxParts || rows < 0 || dv < 1 || dv > kMaxDv) return ELSA_ERR_SHAPE;
   if (part_stride < rows) return ELSA_ERR_SHAPE;
   if (!m || !S || !W) return ELSA_ERR_SHAPE;
   if (finalize ? !y : (!m_out || !S_out || !W_out)) return ELSA_ERR_SHAPE;
@@ -901,7 +942,7 @@ int elsa_merge_peers_f32(const float* const* m_ptrs, const float* const* S_ptrs,
   if (!m_ptrs || !S_ptrs || !W_ptrs || !y) return ELSA_ERR_SHAPE;
   if (ranks < 1 || ranks > kMaxPeers || per_rank < 1 || ranks * per_rank > kMergeMaxParts)
     return ELSA_ERR_SHAPE;
-  if (dv < 1 || dv > 64 || rows < 0 || row_lo < 0 || rows_total < row_lo + rows) return ELSA_ERR_SHAPE;
+  if (dv < 1 || dv > kMaxDv || rows < 0 || row_lo < 0 || rows_total < row_lo + rows) return ELSA_ERR_SHAPE;
   if (rows == 0) return ELSA_OK;
   DeviceCache* dc = nullptr;
   if (int st = current_device_cache(&dc)) return st;
@@ -930,7 +971,8 @@ int elsa_merge_peers_f32(const float* const* m_ptrs, const float* const* S_ptrs,
               : parts <= 8  ? merge_peers_kernel<8>
               : parts <= 16 ? merge_peers_kernel<16>
                             : merge_peers_kernel<32>;
-  kern<<<unsigned(blocks), kWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(mp);
+  const dim3 grid{unsigned(blocks), unsigned(dv_slices(dv)), 1u};
+  kern<<<grid, kWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(mp);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "peer merge launch");
   ++t_last_launches;
   return ELSA_OK;
@@ -988,7 +1030,7 @@ int elsa_blockwise_f32(const float* q, const float* k, const float* v, const els
 }
 
 size_t elsa_block_scan_workspace_bytes(int64_t rows, int nblocks, int dv) {
-  if (rows < 0 || nblocks < 1 || dv < 1 || dv > 64) return 0;
+  if (rows < 0 || nblocks < 1 || dv < 1 || dv > kMaxDv) return 0;
   int64_t kp = 1;
   while (kp < nblocks) kp <<= 1;
   return size_t(rows) * size_t(kp) * size_t(2 + dv) * sizeof(float);
@@ -999,7 +1041,7 @@ int elsa_block_scan_f32(const float* m, const float* S, const float* W, int64_t 
                         float* pre_S, float* pre_W, void* workspace, size_t ws_bytes,
                         void* stream) {
   t_last_launches = 0;
-  if (rows < 0 || nblocks < 1 || dv < 1 || dv > 64) return ELSA_ERR_SHAPE;
+  if (rows < 0 || nblocks < 1 || dv < 1 || dv > kMaxDv) return ELSA_ERR_SHAPE;
   if (!m || !S || !W || !total_m || !total_S || !total_W) return ELSA_ERR_SHAPE;
   const bool pre = pre_m || pre_S || pre_W;
   if (pre && !(pre_m && pre_S && pre_W)) return ELSA_ERR_SHAPE;

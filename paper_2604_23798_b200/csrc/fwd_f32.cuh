@@ -151,7 +151,7 @@ __device__ __forceinline__ void trace_mark(const FwdParams& p, int warp, int t, 
 #endif
 }
 
-template <int W_, int TK_, int STAGES_, int R_>
+template <int W_, int TK_, int STAGES_, int R_, int D_ = 64, int DV_ = 64>
 struct FwdTraits {
   static constexpr int W = W_;
   static constexpr int TK = TK_;
@@ -159,8 +159,10 @@ struct FwdTraits {
   static constexpr int R = R_;            // query rows per lane
   static constexpr int RP = R / 2;        // row pairs per lane
   static constexpr int WR = 2 * R;        // query rows per warp
-  static constexpr int D = 64;
-  static constexpr int DV = 64;
+  static constexpr int D = D_;            // padded head width of Q/K (64, or 128 for 64 < d <= 128)
+  static constexpr int DV = DV_;          // V columns per CTA (64 or 128); wider V runs as slices (grid z)
+  static constexpr int CV = DV / 16;      // GEMM2 columns per lane: 4g + 64v + c, v < DV/64, c < 4
+  static constexpr int NV4 = DV / 64;     // float4 V loads per key per lane
   static constexpr int TQ = WR * W;
   static constexpr int QP = D + 4;        // raw Q / K row pitch in floats (272 B; TMA box width)
   static constexpr int QTP = TQ;          // Q^T pitch: Qt[d][row position]
@@ -170,14 +172,21 @@ struct FwdTraits {
   static constexpr int QT_FLOATS = D * QTP;
   static constexpr int K_FLOATS = TK * QP;
   static constexpr int V_FLOATS = TK * VP;
-  static constexpr int P_FLOATS = W * TK * PTP;  // also the raw-Q TMA landing zone
+  // P^T in two key halves (GEMM2 of the first half runs before the second
+  // half is stored) when the whole-tile P area would not fit next to a
+  // 128-wide V ring and a 128-wide Q^T
+  static constexpr bool kHalfP =
+      size_t(D * TQ + STAGES * (TK * (D + 4) + TK * DV) + W * TK * PTP) * 4 + 64 > 227 * 1024;
+  static constexpr int PH = kHalfP ? 2 : 1;  // P passes per tile
+  static constexpr int P_FLOATS = W * (TK / PH) * PTP;  // also the raw-Q TMA landing zone
   static constexpr int QRAW_FLOATS = TQ * QP;
   // Warp specialisation. R = 8: one producer warp, registers uniform.
   // R = 16: a whole producer warpgroup (4 warps, only one issues TMA) so that
   // setmaxnreg can move registers from producers to consumers — the register
   // file is split per SM sub-partition (16K entries each, warps assigned
   // round-robin), so 9 warps would cap every warp at 168 registers.
-  static constexpr bool kRegSplit = R >= 16;
+  // DV = 128: the 128-column W accumulator needs the same register split.
+  static constexpr bool kRegSplit = R >= 16 || DV > 64;
   static constexpr int PRODUCER_WARPS = kRegSplit ? 4 : 1;
   static constexpr int THREADS = (W + PRODUCER_WARPS) * 32;
   static constexpr int MIN_CTAS = (W <= 4 && R <= 8) ? 2 : 1;
@@ -202,15 +211,22 @@ struct FwdTraits {
   // or the .inc blocks forever (240/32 hung on B200)
   static_assert(!kRegSplit || (W / 4) * (CONSUMER_REGS - MAX_REGS) <= MAX_REGS - PRODUCER_REGS,
                 "setmaxnreg growth exceeds the registers the producers release");
+  // Where the raw Q box lands before the transpose: the P area when it fits
+  // (d <= 64); for the wide-Q kernel the K ring (the producer then waits on a
+  // "Q consumed" barrier before its first K/V load).
+  static constexpr bool kQrawInK = QRAW_FLOATS > P_FLOATS;
   static constexpr size_t BAR_OFFSET =
       size_t(QT_FLOATS + STAGES * (K_FLOATS + V_FLOATS) + P_FLOATS) * 4;
-  static constexpr size_t SMEM_BYTES = BAR_OFFSET + (2 * STAGES + 1) * 8;
+  static constexpr size_t SMEM_BYTES = BAR_OFFSET + (2 * STAGES + 2) * 8;
   static constexpr uint32_t KV_TX_BYTES = uint32_t(K_FLOATS + V_FLOATS) * 4;
   static constexpr uint32_t Q_TX_BYTES = uint32_t(QRAW_FLOATS) * 4;
   static_assert(TK % 16 == 0, "TK must be a multiple of 16");
   static_assert(R % 4 == 0, "R must be a multiple of 4 (float4 row groups)");
+  static_assert(DV == 64 || DV == 128, "V slice width");
+  static_assert(RK % PH == 0, "P halves split the lane's GEMM1 keys evenly");
   static_assert(TQ <= 256, "TMA box rows <= 256");
-  static_assert(QRAW_FLOATS <= P_FLOATS, "raw Q must fit the P area");
+  static_assert(QRAW_FLOATS <= P_FLOATS || QRAW_FLOATS <= STAGES * K_FLOATS,
+                "raw Q must fit the P area or the K ring");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert((QT_FLOATS * 4) % 128 == 0 && (K_FLOATS * 4) % 128 == 0 &&
                     (V_FLOATS * 4) % 128 == 0,
@@ -220,8 +236,9 @@ struct FwdTraits {
 template <class T>
 __device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw, float* Ks,
                                                  float* Vs, uint64_t* full, uint64_t* empty,
-                                                 uint64_t* qbar, int b, int h, int q0,
-                                                 int split_lo, int ntiles, int lane) {
+                                                 uint64_t* qbar, uint64_t* qfree, int b, int h,
+                                                 int q0, int col0, int split_lo, int ntiles,
+                                                 int lane) {
   // Plain-load fallback for operands TMA cannot describe (misaligned base or
   // strides, zero strides). Same smem layout as the TMA boxes, zero-filled.
   const float* qg = p.q + int64_t(b) * p.qs_b + int64_t(h) * p.qs_h;
@@ -234,6 +251,7 @@ __device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw
   __threadfence_block();
   __syncwarp();
   if (lane == 0) ptx::mbar_arrive(qbar);
+  if constexpr (T::kQrawInK) ptx::mbar_wait(qfree, 0);  // raw Q sits in the K ring until transposed
   const float* kg = p.k + int64_t(b) * p.ks_b + int64_t(h) * p.ks_h;
   const float* vg = p.v + int64_t(b) * p.vs_b + int64_t(h) * p.vs_h;
   for (int t = 0; t < ntiles; ++t) {
@@ -251,7 +269,7 @@ __device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw
     for (int idx = lane; idx < T::V_FLOATS; idx += 32) {
       const int r = idx / T::VP, c = idx - r * T::VP;
       float val = 0.f;
-      if (c < p.dv && key0 + r < p.n_kv) val = vg[int64_t(key0 + r) * p.vs_r + c];
+      if (col0 + c < p.dv && key0 + r < p.n_kv) val = vg[int64_t(key0 + r) * p.vs_r + col0 + c];
       vs[idx] = val;
     }
     __threadfence_block();
@@ -264,12 +282,12 @@ __device__ __forceinline__ float f4(const float4& v, int c) {
   return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
-template <int W_, int TK_, int STAGES_, int R_, bool kTMA>
-__global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
+template <int W_, int TK_, int STAGES_, int R_, bool kTMA, int D_ = 64, int DV_ = 64>
+__global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS))
     fwd_f32_kernel(const __grid_constant__ FwdParams p, const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV) {
-  using T = FwdTraits<W_, TK_, STAGES_, R_>;
+  using T = FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>;
   constexpr int TK = T::TK, QP = T::QP, QTP = T::QTP, VP = T::VP, PTP = T::PTP, RK = T::RK;
   constexpr int R = T::R, RP = T::RP, WR = T::WR;
   using ptx::f32x2;
@@ -279,10 +297,12 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
   float* Ks = Qt + T::QT_FLOATS;
   float* Vs = Ks + T::STAGES * T::K_FLOATS;
   float* Ps = Vs + T::STAGES * T::V_FLOATS;
-  float* Qraw = Ps;  // raw Q lands in the P area and is transposed out before first use of P
+  // raw Q lands in the P area (or the K ring) and is transposed out before first use
+  float* Qraw = T::kQrawInK ? Ks : Ps;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + T::BAR_OFFSET);
   uint64_t* empty = full + T::STAGES;
   uint64_t* qbar = empty + T::STAGES;
+  uint64_t* qfree = qbar + 1;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -294,6 +314,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
   const int b = bh / p.H;
   const int h = bh - b * p.H;
   const int q0 = qtile * T::TQ;
+  const int col0 = int(blockIdx.z) * T::DV;  // this CTA's column slice of V / W / Y
 
   const int64_t lo64 = int64_t(p.kv_begin) + int64_t(split) * p.split_keys;
   const int split_lo = int(lo64 < p.kv_end ? lo64 : p.kv_end);
@@ -307,6 +328,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
       ptx::mbar_init(&empty[s], T::W);
     }
     ptx::mbar_init(qbar, 1);
+    if constexpr (T::kQrawInK) ptx::mbar_init(qfree, T::W);
     ptx::fence_barrier_init();
   }
   __syncthreads();
@@ -324,17 +346,19 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
         ptx::prefetch_tmap(&tmV);
         ptx::mbar_arrive_expect_tx(qbar, T::Q_TX_BYTES);
         ptx::tma_load_4d(Qraw, &tmQ, qbar, 0, q0, h, b);
+        if constexpr (T::kQrawInK) ptx::mbar_wait(qfree, 0);
         for (int t = 0; t < ntiles; ++t) {
           const int s = t % T::STAGES;
           if (t >= T::STAGES) ptx::mbar_wait_backoff(&empty[s], ((t / T::STAGES) - 1) & 1, ELSA_PRODUCER_SLEEP_NS);
           const int key0 = split_lo + t * TK;
           ptx::mbar_arrive_expect_tx(&full[s], T::KV_TX_BYTES);
           ptx::tma_load_4d(Ks + s * T::K_FLOATS, &tmK, &full[s], 0, key0, h, b);
-          ptx::tma_load_4d(Vs + s * T::V_FLOATS, &tmV, &full[s], 0, key0, h, b);
+          ptx::tma_load_4d(Vs + s * T::V_FLOATS, &tmV, &full[s], col0, key0, h, b);
         }
       }
     } else {
-      producer_generic<T>(p, Qraw, Ks, Vs, full, empty, qbar, b, h, q0, split_lo, ntiles, lane);
+      producer_generic<T>(p, Qraw, Ks, Vs, full, empty, qbar, qfree, b, h, q0, col0, split_lo,
+                          ntiles, lane);
     }
     return;
   }
@@ -368,44 +392,54 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
       dst[(4 * c + 3) * QTP] = v.w * sgn;
     }
   }
-  // every consumer warp must finish reading raw Q before any warp writes P over it
-  asm volatile("bar.sync 1, %0;" ::"r"(T::W * 32) : "memory");
+  if constexpr (T::kQrawInK) {
+    // raw Q occupies the K ring: hand it back to the producer
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(qfree);
+  } else {
+    // every consumer warp must finish reading raw Q before any warp writes P over it
+    asm volatile("bar.sync 1, %0;" ::"r"(T::W * 32) : "memory");
+  }
 
   const float* qt = Qt + warp * WR + rg * R;
-  float* pw = Ps + warp * TK * PTP;
+  float* pw = Ps + warp * (TK / T::PH) * PTP;
   const float* ptr = pw + rg * R;
   const float c2 = p.c;  // |scale| * log2(e) > 0
   const f32x2 cc = ptx::pack2(c2, c2);
 
   // Row pairs: lane rows (rg + 2i), i = 0..R-1, are held as R/2 packed pairs
   // ip = (i = 2ip, 2ip+1), so every GEMM FMA is an FFMA2 outer-product step.
-  f32x2 o2[RP][4];  // W accumulator: [row pair][column 4g + c]
+  constexpr int CV = T::CV;
+  f32x2 o2[RP][CV];  // W accumulator: [row pair][column 4g + 64(c / 4) + c % 4]
   float mrow[R];    // running anchors (log2 units)
   f32x2 l2[RP];     // running normalizer partials (this lane's keys)
 #pragma unroll
   for (int ip = 0; ip < RP; ++ip) {
     l2[ip] = 0ull;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) o2[ip][c] = 0ull;
+    for (int c = 0; c < CV; ++c) o2[ip][c] = 0ull;
   }
 #pragma unroll
   for (int i = 0; i < R; ++i) mrow[i] = -CUDART_INF_F;
 
   // ---- GEMM2 of tile tt: W += P V on FFMA2, o2[ip][c] += v_j[c] (bcast) *
-  // Pt[j][row pair ip]; then release the tile's K/V stage to the producer.
-  auto gemm2_release = [&](int tt) {
+  // Pt[j][row pair ip] over the keys [k0, k0 + TK / PH) whose P^T is in the
+  // P area (rows jj - k0)
+  auto gemm2 = [&](int tt, int k0) {
     const int st = tt % T::STAGES;
     const float* vs = Vs + st * T::V_FLOATS + 4 * g;
 #pragma unroll(T::G2_UNROLL)
-    for (int jj = 0; jj < TK; ++jj) {
+    for (int jj = 0; jj < TK / T::PH; ++jj) {
       f32x2 pr[RP];
 #pragma unroll
       for (int u = 0; u < RP / 2; ++u)
         ptx::lds128x2(ptr + jj * PTP + 4 * u, pr[2 * u], pr[2 * u + 1]);
-      const float4 vf = ptx::lds128(vs + jj * VP);
+      float4 vf[T::NV4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float vv = f4(vf, c);
+      for (int q = 0; q < T::NV4; ++q) vf[q] = ptx::lds128(vs + (k0 + jj) * VP + 64 * q);
+#pragma unroll
+      for (int c = 0; c < CV; ++c) {
+        const float vv = f4(vf[c / 4], c % 4);
         const f32x2 vb = ptx::pack2(vv, vv);
 #pragma unroll
         for (int u = 0; u < RP; ++u) {
@@ -414,9 +448,50 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
         }
       }
     }
+  };
+  // ... then release the tile's K/V stage to the producer.
+  auto gemm2_release = [&](int tt) {
+    const int st = tt % T::STAGES;
+    if constexpr (T::NV4 == 1 && T::PH == 1) {
+      // the d <= 64 / dv <= 64 kernels: this exact form (ptxas schedules the
+      // generalised loop differently)
+      const float* vs = Vs + st * T::V_FLOATS + 4 * g;
+#pragma unroll(T::G2_UNROLL)
+      for (int jj = 0; jj < TK; ++jj) {
+        f32x2 pr[RP];
+#pragma unroll
+        for (int u = 0; u < RP / 2; ++u)
+          ptx::lds128x2(ptr + jj * PTP + 4 * u, pr[2 * u], pr[2 * u + 1]);
+        const float4 vf = ptx::lds128(vs + jj * VP);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float vv = f4(vf, c);
+          const f32x2 vb = ptx::pack2(vv, vv);
+#pragma unroll
+          for (int u = 0; u < RP; ++u) {
+            const int ip = (ELSA_SNAKE && (c & 1)) ? RP - 1 - u : u;
+            ptx::ffma2(o2[ip][c], vb, pr[ip]);
+          }
+        }
+      }
+    } else {
+      gemm2(tt, (T::PH - 1) * (TK / T::PH));
+    }
     __syncwarp();
     trace_mark(p, warp, tt, 4);
     if (lane == 0) ptx::mbar_arrive(&empty[st]);
+  };
+  // P^T of the lane's GEMM1 keys j in [j0, j1): key-major, this lane's R rows
+  // contiguous -> R/4 STS.128 per key; P area row = key - key offset of the pass
+  auto store_p = [&](const f32x2 (&s2)[RP][RK], int j0, int j1) {
+#pragma unroll
+    for (int j = j0; j < j1; ++j) {
+      float* dst = pw + (g + 16 * j - 16 * j0) * PTP + rg * R;
+#pragma unroll
+      for (int u = 0; u < RP / 2; ++u)
+        *reinterpret_cast<ulonglong2*>(dst + 4 * u) =
+            make_ulonglong2(s2[2 * u][j], s2[2 * u + 1][j]);
+    }
   };
 
   // Phase offset between the two warps that share an SM sub-partition (warps
@@ -514,16 +589,26 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
       }
       l2[ip] = ptx::ffma2r(l2[ip], corr, ps);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) o2[ip][c] = ptx::fmul2(o2[ip][c], corr);
+      for (int c = 0; c < CV; ++c) o2[ip][c] = ptx::fmul2(o2[ip][c], corr);
     }
-    // P^T: key-major, this lane's R rows contiguous -> R/4 STS.128 per key
+    if constexpr (T::kHalfP) {
+      // first key half through the (half-size) P area, then the second half
+      static_assert(!T::kLag, "halved P assumes the in-order GEMM2");
+      store_p(s2, 0, RK / 2);
+      __syncwarp();
+      gemm2(t, 0);
+      __syncwarp();  // every lane is done reading the first half
+      store_p(s2, RK / 2, RK);
+    } else {
+      // P^T: key-major, this lane's R rows contiguous -> R/4 STS.128 per key
 #pragma unroll
-    for (int j = 0; j < RK; ++j) {
-      float* dst = pw + (g + 16 * j) * PTP + rg * R;
+      for (int j = 0; j < RK; ++j) {
+        float* dst = pw + (g + 16 * j) * PTP + rg * R;
 #pragma unroll
-      for (int u = 0; u < RP / 2; ++u)
-        *reinterpret_cast<ulonglong2*>(dst + 4 * u) =
-            make_ulonglong2(s2[2 * u][j], s2[2 * u + 1][j]);
+        for (int u = 0; u < RP / 2; ++u)
+          *reinterpret_cast<ulonglong2*>(dst + 4 * u) =
+              make_ulonglong2(s2[2 * u][j], s2[2 * u + 1][j]);
+      }
     }
     __syncwarp();
     trace_mark(p, warp, t, 3);
@@ -542,9 +627,9 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
       l += __shfl_xor_sync(0xffffffffu, l, 2);
       l += __shfl_xor_sync(0xffffffffu, l, 4);
       l += __shfl_xor_sync(0xffffffffu, l, 16);
-      float o[4];
+      float o[CV];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) o[c] = half ? ptx::hi2(o2[ip][c]) : ptx::lo2(o2[ip][c]);
+      for (int c = 0; c < CV; ++c) o[c] = half ? ptx::hi2(o2[ip][c]) : ptx::lo2(o2[ip][c]);
       const int qrow = q0 + warp * WR + rg + 2 * i;
       if (qrow >= p.n_q) continue;
       if (p.mode == kModeFinal) {
@@ -553,33 +638,41 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_>::MAX_REGS))
           if (g == 0) atomicCAS(p.err, 0, 3);
         }
         float* yrow = p.y + int64_t(b) * p.ys_b + int64_t(h) * p.ys_h + int64_t(qrow) * p.ys_r;
-        float yv[4];
+        float yv[CV];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) yv[c] = __fdiv_rn(o[c], l);
-        const int col = 4 * g;
-        if (p.y_vec && col + 3 < p.dv) {
-          *reinterpret_cast<float4*>(yrow + col) = make_float4(yv[0], yv[1], yv[2], yv[3]);
-        } else {
+        for (int c = 0; c < CV; ++c) yv[c] = __fdiv_rn(o[c], l);
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (col + c < p.dv) yrow[col + c] = yv[c];
+        for (int v4 = 0; v4 < T::NV4; ++v4) {
+          const int col = col0 + 64 * v4 + 4 * g;
+          const float* yq = yv + 4 * v4;
+          if (p.y_vec && col + 3 < p.dv) {
+            *reinterpret_cast<float4*>(yrow + col) = make_float4(yq[0], yq[1], yq[2], yq[3]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (col + c < p.dv) yrow[col + c] = yq[c];
+          }
         }
       } else {
         const int64_t row = int64_t(bh_rel) * p.n_q + qrow;  // relative to this batch
         const int64_t idx = int64_t(split) * p.part_stride + row * p.row_stride;
-        if (g == 0) {
+        if (g == 0 && col0 == 0) {  // m and S are the same in every column slice
           const float m = (p.mode == kModePartialNat) ? mrow[i] * 0.69314718055994531f : mrow[i];
           p.pm[idx] = m;
           p.pS[idx] = l;
         }
         float* wrow = p.pW + idx * p.pw_pitch;
-        const int col = 4 * g;
-        if (p.pw_vec && col + 3 < p.dv) {
-          *reinterpret_cast<float4*>(wrow + col) = make_float4(o[0], o[1], o[2], o[3]);
-        } else {
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (col + c < p.dv) wrow[col + c] = o[c];
+        for (int v4 = 0; v4 < T::NV4; ++v4) {
+          const int col = col0 + 64 * v4 + 4 * g;
+          const float* oq = o + 4 * v4;
+          if (p.pw_vec && col + 3 < p.dv) {
+            *reinterpret_cast<float4*>(wrow + col) = make_float4(oq[0], oq[1], oq[2], oq[3]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (col + c < p.dv) wrow[col + c] = oq[c];
+          }
         }
       }
     }

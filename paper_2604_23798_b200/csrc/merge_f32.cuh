@@ -11,7 +11,9 @@
 //                                                  up-sweep on 2^k inputs, engine.py:179-199)
 //   finalize: Y = W / S with S finite and > 0       engine.py:375-382
 //
-// One warp per query row; lane c owns W columns c and c+32 (dv <= 64). The
+// One warp per query row and 64-column slice (grid y; wider dv runs as
+// several slices that recompute the same m/S tree); lane c owns columns
+// 64y + c and 64y + c + 32. The
 // tree lives in registers (MAXP slots, fully unrolled, predicated on the live
 // count) so the reduction order is fixed by `parts` alone: bitwise
 // deterministic and independent of scheduling.
@@ -95,7 +97,7 @@ __global__ void __launch_bounds__(256) merge_f32_kernel(const MergeParams p) {
   const bool lg = p.log2_domain != 0;
 
   float am[MAXP], aS[MAXP], a0[MAXP], a1[MAXP];
-  const int c0 = lane, c1 = lane + 32;
+  const int c0 = int(blockIdx.y) * 64 + lane, c1 = c0 + 32;
 #pragma unroll
   for (int i = 0; i < MAXP; ++i) {
     if (i < p.parts) {
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(256) merge_f32_kernel(const MergeParams p) {
     if (c0 < p.dv) yrow[c0] = __fdiv_rn(a0[0], s);
     if (c1 < p.dv) yrow[c1] = __fdiv_rn(a1[0], s);
   } else {
-    if (lane == 0) {
+    if (lane == 0 && blockIdx.y == 0) {
       p.m_out[row] = p.out_log2_to_nat ? am[0] * 0.69314718055994531f : am[0];
       p.S_out[row] = aS[0];
     }
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(256) merge_peers_kernel(const PeerMergeParams 
   const int64_t row = p.row_lo + r;
   const int parts = p.ranks * p.per_rank;
   float am[MAXP], aS[MAXP], a0[MAXP], a1[MAXP];
-  const int c0 = lane, c1 = lane + 32;
+  const int c0 = int(blockIdx.y) * 64 + lane, c1 = c0 + 32;
 #pragma unroll
   for (int i = 0; i < MAXP; ++i) {
     if (i < parts) {

@@ -209,7 +209,7 @@ def _precision_name(p):
     return getattr(p, "value", str(p)).lower()
 
 
-def analytic_trace(b, h, n, block_size, splits, workspace_bytes=None):
+def analytic_trace(b, h, n, block_size, splits, workspace_bytes=None, d_v=64):
     """ScanTrace of the GPU schedule for a (b, h, n) problem run with
     ``splits`` KV splits (see :class:`ScanTrace`); ``workspace_bytes`` is the
     split workspace the library asked for (elsa_workspace_bytes), else the
@@ -223,7 +223,7 @@ def analytic_trace(b, h, n, block_size, splits, workspace_bytes=None):
         per_level_counts=[paths * tiles] + ([paths * (splits - 1)] if splits > 1 else []),
         leaf_count=b * h * n * n,
         peak_extra_memory=(int(workspace_bytes) if workspace_bytes is not None
-                           else (splits * b * h * n * (2 + 64) * 4) if splits > 1 else 0),
+                           else (splits * b * h * n * (2 + 64 * -(-d_v // 64)) * 4) if splits > 1 else 0),
         n_paths=paths,
         schedule_depth=4 + tps + _clog2(splits),
         kv_splits=splits,

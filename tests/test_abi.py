@@ -83,7 +83,7 @@ def test_split_planner():
 
 
 @pytest.mark.parametrize("bad", [
-    dict(d=65), dict(dv=0), dict(d=0), dict(n_kv=0),
+    dict(d=129), dict(dv=4097), dict(dv=0), dict(d=0), dict(n_kv=0),
 ])
 def test_invalid_shapes_rejected_without_touching_the_gpu(bad):
     kw = dict(B=1, H=1, n_q=8, n_kv=8, d=64, dv=64)
@@ -112,8 +112,21 @@ def test_bad_scale_and_ranges_rejected():
                             None) == _lib.ELSA_ERR_SHAPE
     assert h.elsa_merge_f32(fake, fake, fake, 33, 4, 8, 4, 1, fake, None, None, None,
                             None) == _lib.ELSA_ERR_SHAPE
-    assert h.elsa_merge_f32(fake, fake, fake, 2, 4, 65, 4, 1, fake, None, None, None,
+    assert h.elsa_merge_f32(fake, fake, fake, 2, 4, 4097, 4, 1, fake, None, None, None,
                             None) == _lib.ELSA_ERR_SHAPE
+    assert h.elsa_merge_f32(fake, fake, fake, 2, 4, 0, 4, 1, fake, None, None, None,
+                            None) == _lib.ELSA_ERR_SHAPE
+
+
+def test_wide_head_workspace_counts_every_column_slice():
+    # dv > 64 runs as ceil(dv / 64) slices; the split workspace keeps
+    # 2 + 64 * slices floats per row per split
+    h = _lib.lib()
+    for d, dv, per_row in ((128, 64, 66), (64, 128, 130), (128, 200, 2 + 256), (96, 1, 66)):
+        ws = h.elsa_workspace_bytes(ctypes.byref(_shape(1, 1, 1024, 1024, d=d, dv=dv)), 4)
+        assert ws == 4 * 1024 * per_row * 4, (d, dv, ws)
+    assert h.elsa_block_scan_workspace_bytes(10, 5, 200) == 10 * 8 * 202 * 4
+    assert h.elsa_block_scan_workspace_bytes(10, 5, 4097) == 0
 
 
 def test_empty_problem_is_a_noop():
