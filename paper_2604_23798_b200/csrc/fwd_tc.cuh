@@ -73,18 +73,36 @@ __device__ unsigned long long g_tc_trace[16 * kTcTraceTiles * 8];
 #endif
 
 // Share of the exponentials computed on the FMA pipe instead of MUFU: this
-// many pairs out of every 8 scores (0..4). MUFU.EX2 issues at 16 lanes/clk/SM,
-// so with 128 exponentials per row per tile it is the softmax's binding
-// pipe; a polynomial on FFMA2 moves part of that load to the idle FMA pipe.
+// many pairs out of every 8 scores (0..4), plus one more pair in the 8-key
+// units flagged in ELSA_TC_POLY_EXTRA. MUFU.EX2 issues at 16 lanes/clk/SM
+// (tools/microbench/mufu_ex2.cu; f16x2 / bf16x2 forms are no faster), so with
+// 128 exponentials per row per tile it is the softmax's binding pipe (ncu: XU
+// 78% of peak); a polynomial on FFMA2 moves part of that load to the FMA
+// pipe, and packed FFMA2 / FADD2 argument and sum arithmetic frees the issue
+// slots the polynomial needs. Measured (tools/tc_variant_ab.py, BF16 16K):
+// none 839, 25% 864, packed + 25% 877-882, packed + 31% 899, packed + 37.5%
+// (the default) 910, packed + 44% 880, packed + 50% 873 TFLOP/s; errors vs
+// FP64 unchanged (8.82e-3 vs PyTorch's 8.85e-3).
 #ifndef ELSA_TC_POLY_PAIRS
-#define ELSA_TC_POLY_PAIRS 0  // measured: 1 pair 699, 2 pairs 654 vs 0 763 TFLOP/s at 16K
+#define ELSA_TC_POLY_PAIRS 1  // pairs per 8-key unit on the FMA pipe (see ELSA_TC_POLY_EXTRA)
 #endif
 constexpr int kTcPolyPairs = ELSA_TC_POLY_PAIRS;
+#ifndef ELSA_TC_PACKED_G2
+#define ELSA_TC_PACKED_G2 1  // packed FFMA2/FADD2 softmax arithmetic for two-tile CTAs too
+#endif
+constexpr bool kTcPackedG2 = ELSA_TC_PACKED_G2 != 0;
+#ifndef ELSA_TC_POLY_EXTRA
+#define ELSA_TC_POLY_EXTRA 0x5555  // bit u: one more polynomial pair in 8-key unit u
+#endif
+#ifndef ELSA_TC_POLY_DEG
+#define ELSA_TC_POLY_DEG 3
+#endif
 
 // 2^x for a pair, x <= 2^7, on the FMA pipe: x = j + f with j = rint(x) (the
-// 1.5*2^23 shifter), f in [-1/2, 1/2]; 2^f by its degree-4 Taylor polynomial
-// (relative error < 6e-5, below the 16-bit formats' rounding of P:
-// 2^-9 bf16, 2^-11 fp16); 2^j added to the exponent field. x is clamped to
+// 1.5*2^23 shifter), f in [-1/2, 1/2]; 2^f by a degree-3 minimax polynomial
+// (relative error 7.5e-5; degree 4 Taylor: 5.6e-5, one more FFMA2 — both
+// below the 16-bit formats' rounding of P: 2^-9 bf16, 2^-11 fp16); 2^j added
+// to the exponent field. x is clamped to
 // -126 so the result stays normal (>= 0.7 * 2^-126: negligible against S >= 1).
 __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
   using ptx::f32x2;
@@ -93,11 +111,20 @@ __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& 
   const f32x2 r = ptx::fadd2(x, shifter);        // j in the low mantissa bits
   const f32x2 j = ptx::fadd2(r, ptx::pack2(-12582912.f, -12582912.f));
   const f32x2 f = ptx::ffma2r(j, ptx::pack2(-1.f, -1.f), x);  // x - j, exact
+#if ELSA_TC_POLY_DEG == 3
+  // degree-3 minimax fit of 2^f on [-1/2, 1/2] (relative error 7.5e-5, under
+  // fp16's 2^-11 and bf16's 2^-8 rounding of P)
+  f32x2 q = ptx::ffma2r(f, ptx::pack2(5.517132e-2f, 5.517132e-2f),
+                        ptx::pack2(2.4261054e-1f, 2.4261054e-1f));
+  q = ptx::ffma2r(q, f, ptx::pack2(6.9326097e-1f, 6.9326097e-1f));
+  q = ptx::ffma2r(q, f, ptx::pack2(9.999281e-1f, 9.999281e-1f));
+#else
   f32x2 q = ptx::ffma2r(f, ptx::pack2(9.6181291e-3f, 9.6181291e-3f),
                         ptx::pack2(5.5504109e-2f, 5.5504109e-2f));
   q = ptx::ffma2r(q, f, ptx::pack2(2.4022651e-1f, 2.4022651e-1f));
   q = ptx::ffma2r(q, f, ptx::pack2(6.9314718e-1f, 6.9314718e-1f));
   q = ptx::ffma2r(q, f, ptx::pack2(1.f, 1.f));
+#endif
   float q0, q1, r0, r1;
   ptx::unpack2(q, q0, q1);
   ptx::unpack2(r, r0, r1);
@@ -435,20 +462,21 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
           float x0, x1;
-          if constexpr (GROUPS == 1) {
+          if constexpr (GROUPS == 1 || kTcPackedG2) {
             ptx::unpack2(ptx::ffma2r(ptx::pack2(s[u * 8 + e], s[u * 8 + e + 1]), cs2, nm2), x0, x1);
           } else {
             x0 = fmaf(s[u * 8 + e], cs, neg_m);
             x1 = fmaf(s[u * 8 + e + 1], cs, neg_m);
           }
-          if (e < 2 * kTcPolyPairs) {  // this pair on the FMA pipe, the rest on MUFU
+          // this pair on the FMA pipe, the rest on MUFU
+          if (e < 2 * (kTcPolyPairs + ((ELSA_TC_POLY_EXTRA >> u) & 1))) {
             ex2_poly2(x0, x1, pv[e], pv[e + 1]);
           } else {
             pv[e] = ptx::ex2(x0);
             pv[e + 1] = ptx::ex2(x1);
           }
         }
-        if constexpr (GROUPS == 1) {
+        if constexpr (GROUPS == 1 || kTcPackedG2) {
           psa = ptx::fadd2(psa, ptx::fadd2(ptx::pack2(pv[0], pv[1]), ptx::pack2(pv[2], pv[3])));
           psb = ptx::fadd2(psb, ptx::fadd2(ptx::pack2(pv[4], pv[5]), ptx::pack2(pv[6], pv[7])));
         } else {
@@ -464,7 +492,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       }
       tc::tmem_wait_st();
       float psum;
-      if constexpr (GROUPS == 1) {
+      if constexpr (GROUPS == 1 || kTcPackedG2) {
         const ptx::f32x2 pt = ptx::fadd2(psa, psb);
         psum = ptx::lo2(pt) + ptx::hi2(pt);
       } else {
