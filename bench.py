@@ -507,6 +507,17 @@ def main():
         cpu = {"value": val, "unit": "TFLOP/s", "cores": workers, "kind": "port",
                "sample": desc, "seconds": secs}
 
+    if sharded and args.shard == "kv":
+        # per-rank working set of one step: all of Q, this rank's K/V shard and
+        # its chunk states (m, S, W for every query row)
+        per = chunks // world
+        ws_mb = (q.numel() + k_loc.numel() + v_loc.numel()
+                 + per * B * H * n * (2 + 64)) * 4 / 1e6
+        l2_note = ("per-rank step working set %.0f MB (Q, K/V shard, chunk states) > 126 MB L2; "
+                   "sweep flushes L2 (256 MB write) between timed iterations" % ws_mb)
+    else:
+        l2_note = ("inputs 3x%.0f MB > 126 MB L2; sweep flushes L2 (256 MB write) "
+                   "between timed iterations" % (q.numel() * 4 / 1e6))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
@@ -517,8 +528,7 @@ def main():
                                    + (f", KV-sharded over {world} GPUs ({chunks} chunks)"
                                       if sharded else ""),
                        "B": B, "H": H, "n": n, "d": 64, "dv": 64,
-                       "l2": "inputs 3x%.0f MB > 126 MB L2; sweep flushes L2 (256 MB write) "
-                             "between timed iterations" % (q.numel() * 4 / 1e6),
+                       "l2": l2_note,
                        "parallelism": f"kv-shard{world}" if sharded else "single GPU",
                        "exchange": (exchange[0] if args.shard == "kv" else "none (query-sharded)")
                                    if sharded else None},
