@@ -33,7 +33,7 @@ using namespace elsa;
 namespace {
 
 constexpr int kMaxDevices = 64;
-constexpr int kAttrSlots = 16;
+constexpr int kAttrSlots = 24;
 constexpr int kMaxSplits = kMergeMaxParts;
 constexpr double kLog2e = 1.4426950408889634074;
 
@@ -109,6 +109,7 @@ int current_device_cache(DeviceCache** out) {
 //          lane (setmaxnreg register split with a producer warpgroup)
 //   w8r8d128: w8r8 with Q/K 128 floats wide (64 < d <= 128; Q^T and the K
 //          ring fill 200 KB, raw Q is staged in the K ring)
+//   w8r8d96, w8r8d96v128: the same with Q/K 96 wide (64 < d <= 96)
 //   w8r8v128, w8r8d128v128: 128 V columns per CTA (dv > 64): a 128-column
 //          W accumulator (setmaxnreg register split with a producer
 //          warpgroup); with d > 64 too, P^T goes through shared memory in
@@ -124,9 +125,13 @@ enum CfgId {
   kCfgW8R8D128 = 3,
   kCfgW8R8V128 = 4,
   kCfgW8R8D128V128 = 5,
+  kCfgW8R8D96 = 6,  // 64 < d <= 96: Q/K 96 wide (GEMM1 3/4 of the d = 128 kernel's)
+  kCfgW8R8D96V128 = 7,
   kCfgAuto = -1
 };
-int cfg_dv(int cfg) { return cfg >= kCfgW8R8V128 ? 128 : 64; }
+int cfg_dv(int cfg) {
+  return (cfg == kCfgW8R8V128 || cfg == kCfgW8R8D128V128 || cfg == kCfgW8R8D96V128) ? 128 : 64;
+}
 constexpr int64_t kMaxD = 128;
 constexpr int64_t kMaxDv = 4096;
 int64_t dv_slices(int64_t dv) { return (dv + 63) / 64; }
@@ -163,6 +168,10 @@ CfgInfo cfg_info(int cfg) {
       return {128, 64, 1, 8.03, 6.2};
     case kCfgW8R8D128V128:
       return {128, 64, 1, 10.7, 8.2};
+    case kCfgW8R8D96:
+      return {128, 64, 1, 6.7, 5.2};
+    case kCfgW8R8D96V128:
+      return {128, 64, 1, 9.4, 7.2};
     default:
       return {64, 64, 2, 2.711, 1.6};
   }
@@ -231,8 +240,9 @@ int64_t normalize_splits(int64_t s, int64_t tiles) {
 Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms) {
   const int64_t BH = sh->B * sh->H;
   // head widths beyond 64 have one configuration each; d, dv <= 64 choose
-  const int wide = (sh->d > 64 ? 1 : 0) | (sh->dv > 64 ? 2 : 0);
-  const int only[4] = {-1, kCfgW8R8D128, kCfgW8R8V128, kCfgW8R8D128V128};
+  const int wide = (sh->d > 64 ? (sh->d > 96 ? 1 : 4) : 0) | (sh->dv > 64 ? 2 : 0);
+  const int only[7] = {-1, kCfgW8R8D128, kCfgW8R8V128, kCfgW8R8D128V128, kCfgW8R8D96, -1,
+                       kCfgW8R8D96V128};
   const int first = wide ? only[wide] : 0, last = wide ? only[wide] + 1 : int(kCfgCount);
   Plan best{first, 1, BH > 0 ? BH : 1};
   double best_t = 1e300;
@@ -366,6 +376,12 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
     case kCfgW8R8D128V128:
       return launch_fwd_cfg<8, 64, 2, 8, 128, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
                                                    kCfgW8R8D128V128, dc, stream);
+    case kCfgW8R8D96:
+      return launch_fwd_cfg<8, 64, 2, 8, 96>(p, s, q_st, k_st, v_st, splits, bh_count,
+                                             kCfgW8R8D96, dc, stream);
+    case kCfgW8R8D96V128:
+      return launch_fwd_cfg<8, 64, 2, 8, 96, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
+                                                  kCfgW8R8D96V128, dc, stream);
     default:
       return launch_fwd_cfg<4, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW4R8, dc,
                                          stream);
