@@ -137,6 +137,9 @@ __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& 
 #endif
 constexpr bool kTcSelfIssue = ELSA_TC_SELF_ISSUE != 0;
 
+#ifndef ELSA_TC_PSPLIT
+#define ELSA_TC_PSPLIT 1  // P_g(t) handed to the tensor core in this many key parts (2: 597, 4: 461 vs 1: 907 TFLOP/s BF16 16K — the mid-loop wait/arrive serialises the exponentials)
+#endif
 #ifndef ELSA_TC_STAGES
 #define ELSA_TC_STAGES 4  // K/V ring depth (measured: 2: 697, 3: 827, 4: 845, 5: 845 TFLOP/s at 16K)
 #endif
@@ -158,7 +161,12 @@ struct TcTraits {
   static constexpr int OFF_BAR = OFF_V + STAGES * V_BYTES;
   // barriers: qbar, kv_full[3], kv_empty[3], s_full[G], s_free[G], p_full[G], o_full[G],
   // + tmem base word
-  static constexpr int NBAR = 1 + 2 * STAGES + 4 * GROUPS;
+  // P and its P V MMAs in PH key parts, each with its own p_full / o_full
+  // barrier: part 0's P V runs while the softmax computes part 1, and the
+  // next tile only waits for part h's P V before overwriting part h of P
+  static constexpr int PH = kTcSelfIssue ? 1 : ELSA_TC_PSPLIT;
+  static_assert(PH == 1 || PH == 2 || PH == 4, "P parts");
+  static constexpr int NBAR = 1 + 2 * STAGES + (2 + 2 * PH) * GROUPS;
   static constexpr size_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16 + 1024;  // + 1024 alignment slack
   static constexpr int SOFTMAX_WARPS = 4 * GROUPS;
   static constexpr int TMA_WARP = SOFTMAX_WARPS, MMA_WARP = SOFTMAX_WARPS + 1;
@@ -197,9 +205,10 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
   uint64_t* kv_empty = kv_full + T::STAGES;
   uint64_t* s_full = kv_empty + T::STAGES;
   uint64_t* s_free = s_full + GROUPS;
-  uint64_t* p_full = s_free + GROUPS;
-  uint64_t* o_full = p_full + GROUPS;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(o_full + GROUPS);
+  uint64_t* p_full = s_free + GROUPS;    // [g * PH + part]
+  uint64_t* o_full = p_full + GROUPS * T::PH;  // [g * PH + part]
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(o_full + GROUPS * T::PH);
+  constexpr int PH = T::PH;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -219,8 +228,10 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     for (int g = 0; g < GROUPS; ++g) {
       ptx::mbar_init(&s_full[g], 1);
       ptx::mbar_init(&s_free[g], 128);
-      ptx::mbar_init(&p_full[g], 128);
-      ptx::mbar_init(&o_full[g], 1);
+      for (int hh = 0; hh < PH; ++hh) {
+        ptx::mbar_init(&p_full[g * PH + hh], 128);
+        ptx::mbar_init(&o_full[g * PH + hh], 1);
+      }
     }
     ptx::fence_barrier_init();
   }
@@ -249,18 +260,21 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     if (leader) tc::commit(&s_full[g]);
     __syncwarp();
   };
-  auto issue_o = [&](int g, int t, bool leader) {  // W_g (+)= P_g(t) V_t, P from TMEM
+  // W_g (+)= P_g(t) V_t over key part hh, P from TMEM
+  auto issue_o = [&](int g, int t, int hh, bool leader) {
     const int s = t % T::STAGES;
     const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V + s * T::V_BYTES);
     const uint32_t d = tmem + T::O_COL + g * 64;
     const uint32_t pa = tmem + T::P_COL + g * 64;
+    constexpr int KS = T::TK / 16 / PH;  // K-steps per part
 #pragma unroll
-    for (int kk = 0; kk < T::TK / 16; ++kk) {
+    for (int k2 = 0; k2 < KS; ++k2) {
+      const int kk = hh * KS + k2;
       // V: MN-major (rows = keys, 128 B each); 16 keys per step = 2 swizzle atoms
       const uint64_t bd = tc::smem_desc_sw128(v_addr + kk * 2048, 16, 1024);
       if (leader) tc::mma_f16_ts(d, pa + kk * 8, bd, kIdescO, (t > 0 || kk > 0) ? 1u : 0u);
     }
-    if (leader) tc::commit(&o_full[g]);
+    if (leader) tc::commit(&o_full[g * PH + hh]);
     __syncwarp();
   };
   // lane 0's view of a barrier phase, broadcast so the schedule stays uniform
@@ -309,18 +323,19 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     // issued by two separate warps, 815 vs 835; one issuing warp per group,
     // 730 vs 837 — a single issuer is best.)
     ptx::mbar_wait(qbar, 0);
-    int ns[GROUPS], npv[GROUPS];  // next S tile / next P V tile per group
-    for (int g = 0; g < GROUPS; ++g) ns[g] = npv[g] = 0;
+    int ns[GROUPS], npv[GROUPS], nph[GROUPS];  // next S tile / next P V tile and part
+    for (int g = 0; g < GROUPS; ++g) ns[g] = npv[g] = nph[g] = 0;
     int kv_released = 0;  // tiles whose K/V stage was handed back
     while (kv_released < ntiles) {
 #pragma unroll
       for (int g = 0; g < GROUPS; ++g) {
-        const int u = npv[g];
-        if (u < ns[g] && ready(&p_full[g], u & 1)) {  // P V first: on the softmax's path
+        const int u = npv[g], hh = nph[g];
+        if (u < ns[g] && ready(&p_full[g * PH + hh], u & 1)) {  // P V first: on the softmax's path
           tc::fence_after_sync();
-          if (lane == 0) TC_MARK(8 + g, u, 1);
-          issue_o(g, u, leader);
-          npv[g] = u + 1;
+          if (lane == 0 && hh == 0) TC_MARK(8 + g, u, 1);
+          issue_o(g, u, hh, leader);
+          nph[g] = hh + 1 == PH ? 0 : hh + 1;
+          npv[g] = hh + 1 == PH ? u + 1 : u;
           int done = npv[0];
 #pragma unroll
           for (int gg = 1; gg < GROUPS; ++gg) done = npv[gg] < done ? npv[gg] : done;
@@ -428,13 +443,16 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       const float m_new = move ? m_tile : m_run;
       const float corr = move ? ptx::ex2(m_run - m_new) : 1.f;  // 0 on the first move
       m_run = m_new;
-      // P_g(t-1) V done: the P tile is free and W_g holds tiles < t
-      if (t > 0) {
+      // anchor moved: wait for all of P_g(t-1) V (W_g then holds tiles < t)
+      // and rescale this warp's W rows in TMEM; otherwise each P part only
+      // waits for its own P V below
+      if (t > 0 && __any_sync(0xffffffffu, move)) {
         if (lane == 0) TC_MARK(warp, t, 3);
-        ptx::mbar_wait(&o_full[g], (t - 1) & 1);
+#pragma unroll
+        for (int hh = 0; hh < PH; ++hh) ptx::mbar_wait(&o_full[g * PH + hh], (t - 1) & 1);
         if (lane == 0) TC_MARK(warp, t, 4);
         tc::fence_after_sync();
-        if (__any_sync(0xffffffffu, move)) {  // rescale this warp's W rows in TMEM
+        {
 #pragma unroll
           for (int ch = 0; ch < 2; ++ch) {
             uint32_t r[32];
@@ -487,8 +505,20 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
         for (int e = 0; e < 4; ++e)
           pk[(u & 3) * 4 + e] = kBF16 ? tc::pack_bf16x2(pv[2 * e], pv[2 * e + 1])
                                       : tc::pack_f16x2(pv[2 * e], pv[2 * e + 1]);
-        if ((u & 3) == 3)  // 32 keys = 16 columns packed: into TMEM
+        constexpr int UPH = 16 / PH;  // 8-key units per P part
+        if ((u & 3) == 3) {  // 32 keys = 16 columns packed: into TMEM
+          if (t > 0 && u % UPH == 3) {  // part's first store: its P V of tile t-1 must be done
+            ptx::mbar_wait(&o_full[g * PH + u / UPH], (t - 1) & 1);
+            tc::fence_after_sync();
+          }
           tc::tmem_st_32x32b_x16(p_tm + (u >> 2) * 16, pk);
+          if (PH > 1 && !kTcSelfIssue && u % UPH == UPH - 1 && u != 15) {
+            // part complete: hand it to the tensor core
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            ptx::mbar_arrive(&p_full[g * PH + u / UPH]);
+          }
+        }
       }
       tc::tmem_wait_st();
       float psum;
@@ -505,19 +535,20 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
         group_sync();
         if (issuer) {
           tc::fence_after_sync();
-          issue_o(g, t, leader);
+          issue_o(g, t, 0, leader);
           if (leader) tc::commit(&kv_empty[t % T::STAGES]);
           __syncwarp();
         }
       } else {
-        ptx::mbar_arrive(&p_full[g]);
+        ptx::mbar_arrive(&p_full[g * PH + PH - 1]);
       }
       if (lane == 0) TC_MARK(warp, t, 5);
     }
     // ---- epilogue: Y = W / S (engine.py:375-382) in the input's 16-bit format ----
     float w[64];
     if (ntiles > 0) {
-      ptx::mbar_wait(&o_full[g], (ntiles - 1) & 1);
+#pragma unroll
+      for (int hh = 0; hh < PH; ++hh) ptx::mbar_wait(&o_full[g * PH + hh], (ntiles - 1) & 1);
       tc::fence_after_sync();
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {

@@ -13,5 +13,6 @@ timeout 300 python tools/time_tc.py > gpurun_out/tc_time_$TAG.txt 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:fwd_f32 -s 2 -c 1 -o gpurun_out/prof_fwd16k_$TAG python tools/prof_fwd.py --n 16384 --reps 3 > gpurun_out/ncu_full_$TAG.log 2>&1
 ./tools/microbench/ffma_variants > gpurun_out/ffma_variants_$TAG.log 2>&1
 
+timeout 300 python tools/time_wide.py 16384 5 > gpurun_out/time_wide_$TAG.txt 2>&1
 timeout 300 python bench.py --dist-path --steps 5 --no-sweep --no-cpu-baseline > gpurun_out/bench_distpath_$TAG.log 2>&1
 echo done
