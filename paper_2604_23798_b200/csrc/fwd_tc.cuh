@@ -446,8 +446,8 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       // anchor moved: wait for all of P_g(t-1) V (W_g then holds tiles < t)
       // and rescale this warp's W rows in TMEM; otherwise each P part only
       // waits for its own P V below
+      if (lane == 0) TC_MARK(warp, t, 3);
       if (t > 0 && __any_sync(0xffffffffu, move)) {
-        if (lane == 0) TC_MARK(warp, t, 3);
 #pragma unroll
         for (int hh = 0; hh < PH; ++hh) ptx::mbar_wait(&o_full[g * PH + hh], (t - 1) & 1);
         if (lane == 0) TC_MARK(warp, t, 4);

@@ -1,7 +1,7 @@
 """Per-tile timeline of K5 in CTA 0 (build: tools/variant_sweep.sh
 "tctrace:-DELSA_TC_TRACE", run with ELSA_LIB_PATH=build/var_tctrace.so).
 Softmax warp points: 0 before s_full wait, 1 S ready, 2 s_free arrived,
-3 before o_full wait, 4 O ready, 5 p_full arrived. MMA slots 8+g: 0 S issue,
+3 row max done, 4 O rescaled (anchor moves only), 5 p_full arrived. MMA slots 8+g: 0 S issue,
 1 PV issue. Prints SM clocks relative to the first stamp."""
 import ctypes
 import os
@@ -34,9 +34,8 @@ for t in range(8, 40):
 # averages over tiles 8..56: durations
 d = lambda w, x, y: np.mean([a[w, t, y] - a[w, t, x] for t in range(8, 56)])
 for w in (0, 1, 4):
-    print(f"warp {w}: wait S {d(w,0,1):7.0f}  ld S {d(w,1,2):6.0f}  max {d(w,2,3):6.0f}  wait O {d(w,3,4):6.0f}  "
-          f"exp/P {d(w,4,5):6.0f}  tile {np.mean(np.diff(a[w, 8:56, 0])):7.0f} clk")
+    print(f"warp {w}: wait S {d(w,0,1):7.0f}  ld S {d(w,1,2):6.0f}  max {d(w,2,3):6.0f}  "
+          f"exp/P (incl. O wait) {d(w,3,5):6.0f}  tile {np.mean(np.diff(a[w, 8:56, 0])):7.0f} clk")
 print("S issue -> S ready (g0):", np.mean([a[0, t, 1] - a[8, t, 0] for t in range(8, 56)]))
-print("PV issue -> O ready (g0):", np.mean([a[0, t + 1, 4] - a[8, t, 1] for t in range(8, 56)]))
 print("p_full -> PV issue (g0):", np.mean([a[8, t, 1] - a[0, t, 5] for t in range(8, 56)]))
 print("s_free -> S issue (g0):", np.mean([a[8, t + 1, 0] - a[0, t, 2] for t in range(8, 56)]))
