@@ -162,6 +162,9 @@ CfgInfo cfg_info(int cfg) {
       return {256, 64, 1, 10.75, 7.6};
     case kCfgW8R8:
       return {128, 64, 1, 5.355, 4.1};
+    // wide-head configurations: scaled from the w8r8 fit by GEMM length
+    // (d + dv relative to 128), not fitted — the planner only compares kv
+    // split counts within one of them
     case kCfgW8R8D128:  // GEMM1 twice as long: ~1.5x the d = 64 tile
       return {128, 64, 1, 8.03, 6.2};
     case kCfgW8R8V128:  // GEMM2 twice as long

@@ -159,7 +159,7 @@ struct FwdTraits {
   static constexpr int R = R_;            // query rows per lane
   static constexpr int RP = R / 2;        // row pairs per lane
   static constexpr int WR = 2 * R;        // query rows per warp
-  static constexpr int D = D_;            // padded head width of Q/K (64, or 128 for 64 < d <= 128)
+  static constexpr int D = D_;            // padded head width of Q/K: 64, 96 or 128
   static constexpr int DV = DV_;          // V columns per CTA (64 or 128); wider V runs as slices (grid z)
   static constexpr int CV = DV / 16;      // GEMM2 columns per lane: 4g + 64v + c, v < DV/64, c < 4
   static constexpr int NV4 = DV / 64;     // float4 V loads per key per lane
@@ -212,7 +212,7 @@ struct FwdTraits {
   static_assert(!kRegSplit || (W / 4) * (CONSUMER_REGS - MAX_REGS) <= MAX_REGS - PRODUCER_REGS,
                 "setmaxnreg growth exceeds the registers the producers release");
   // Where the raw Q box lands before the transpose: the P area when it fits
-  // (d <= 64); for the wide-Q kernel the K ring (the producer then waits on a
+  // (d <= 64); for the wide-Q kernels the K ring (the producer then waits on a
   // "Q consumed" barrier before its first K/V load).
   static constexpr bool kQrawInK = QRAW_FLOATS > P_FLOATS;
   static constexpr size_t BAR_OFFSET =
