@@ -54,8 +54,8 @@ typedef enum {
 
 /* Problem geometry. Q:(B,H,n_q,d) K:(B,H,n_kv,d) V:(B,H,n_kv,dv) Y:(B,H,n_q,dv).
  * Strides are in ELEMENTS for the (b, h, row) axes; the last axis of every
- * tensor must be contiguous (stride 1). d <= 128, dv <= 4096 (V wider than 64
- * runs as 64-column slices). */
+ * tensor must be contiguous (stride 1). d <= 256, dv <= 4096 (V wider than the
+ * kernel's 64 / 128 columns runs as column slices). */
 typedef struct {
   int64_t B, H, n_q, n_kv, d, dv;
   int64_t q_stride[3];

@@ -41,8 +41,8 @@ __all__ = [
 
 
 # Widest heads the FP32 kernels take (elsa_abi.cu kMaxD / kMaxDv): Q/K up to
-# 128 floats wide; V of any width up to 4096 as 64-column slices.
-MAX_D = 128
+# 256 floats wide; V of any width up to 4096 as column slices.
+MAX_D = 256
 MAX_DV = 4096
 
 def _stream_ptr(device):

@@ -110,6 +110,9 @@ int current_device_cache(DeviceCache** out) {
 //   w8r8d128: w8r8 with Q/K 128 floats wide (64 < d <= 128; Q^T and the K
 //          ring fill 200 KB, raw Q is staged in the K ring)
 //   w8r8d96, w8r8d96v128: the same with Q/K 96 wide (64 < d <= 96)
+//   w4r8d256, w4r8d256v128: 128 < d <= 256: 4 consumer warps x 16 rows
+//          (TQ = 64), 32-key tiles, plain loads (TMA boxes stop at 256
+//          elements, the padded pitch is 260), 1 CTA / SM
 //   w8r8v128, w8r8d128v128: 128 V columns per CTA (dv > 64): a 128-column
 //          W accumulator (setmaxnreg register split with a producer
 //          warpgroup); with d > 64 too, P^T goes through shared memory in
@@ -127,12 +130,25 @@ enum CfgId {
   kCfgW8R8D128V128 = 5,
   kCfgW8R8D96 = 6,  // 64 < d <= 96: Q/K 96 wide (GEMM1 3/4 of the d = 128 kernel's)
   kCfgW8R8D96V128 = 7,
+  kCfgW4R8D256 = 8,  // 128 < d <= 256: 4 consumer warps, 32-key tiles, plain loads
+  kCfgW4R8D256V128 = 9,
   kCfgAuto = -1
 };
 int cfg_dv(int cfg) {
-  return (cfg == kCfgW8R8V128 || cfg == kCfgW8R8D128V128 || cfg == kCfgW8R8D96V128) ? 128 : 64;
+  return (cfg == kCfgW8R8V128 || cfg == kCfgW8R8D128V128 || cfg == kCfgW8R8D96V128 ||
+          cfg == kCfgW4R8D256V128)
+             ? 128
+             : 64;
 }
-constexpr int64_t kMaxD = 128;
+// the one configuration for heads wider than 64 (-1: choose among the d <= 64 ones)
+int wide_cfg(int64_t d, int64_t dv) {
+  const bool v = dv > 64;
+  if (d <= 64) return v ? int(kCfgW8R8V128) : -1;
+  if (d <= 96) return v ? int(kCfgW8R8D96V128) : int(kCfgW8R8D96);
+  if (d <= 128) return v ? int(kCfgW8R8D128V128) : int(kCfgW8R8D128);
+  return v ? int(kCfgW4R8D256V128) : int(kCfgW4R8D256);
+}
+constexpr int64_t kMaxD = 256;
 constexpr int64_t kMaxDv = 4096;
 int64_t dv_slices(int64_t dv) { return (dv + 63) / 64; }
 
@@ -175,6 +191,10 @@ CfgInfo cfg_info(int cfg) {
       return {128, 64, 1, 6.7, 5.2};
     case kCfgW8R8D96V128:
       return {128, 64, 1, 9.4, 7.2};
+    case kCfgW4R8D256:  // 64 x 32 tiles
+      return {64, 32, 1, 4.0, 4.0};
+    case kCfgW4R8D256V128:
+      return {64, 32, 1, 5.0, 4.0};
     default:
       return {64, 64, 2, 2.711, 1.6};
   }
@@ -243,10 +263,9 @@ int64_t normalize_splits(int64_t s, int64_t tiles) {
 Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms) {
   const int64_t BH = sh->B * sh->H;
   // head widths beyond 64 have one configuration each; d, dv <= 64 choose
-  const int wide = (sh->d > 64 ? (sh->d > 96 ? 1 : 4) : 0) | (sh->dv > 64 ? 2 : 0);
-  const int only[7] = {-1, kCfgW8R8D128, kCfgW8R8V128, kCfgW8R8D128V128, kCfgW8R8D96, -1,
-                       kCfgW8R8D96V128};
-  const int first = wide ? only[wide] : 0, last = wide ? only[wide] + 1 : int(kCfgCount);
+  const int only = wide_cfg(sh->d, sh->dv);
+  const bool wide = only >= 0;
+  const int first = wide ? only : 0, last = wide ? only + 1 : int(kCfgCount);
   Plan best{first, 1, BH > 0 ? BH : 1};
   double best_t = 1e300;
   const int forced = wide ? int(kCfgAuto) : forced_cfg();
@@ -332,7 +351,17 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
 
   CUtensorMap maps[3];
   std::memset(maps, 0, sizeof(maps));
-  bool use_tma = tma_ok(p.q, q_st, s->d) && tma_ok(p.k, k_st, s->d) && tma_ok(p.v, v_st, s->dv);
+  // copy engine (non-TMA) alignment: 16-byte copies when base and strides allow
+  auto vec_ok = [](const float* base, const int64_t st[3]) {
+    return reinterpret_cast<uintptr_t>(base) % 16 == 0 && st[0] % 4 == 0 && st[1] % 4 == 0 &&
+           st[2] % 4 == 0;
+  };
+  p.q_vec = vec_ok(p.q, q_st);
+  p.k_vec = vec_ok(p.k, k_st);
+  p.v_vec = vec_ok(p.v, v_st);
+  // TMA boxes are at most 256 elements wide: the d = 256 kernel (pitch 260) uses the copy engine
+  bool use_tma = T::QP <= 256 && tma_ok(p.q, q_st, s->d) && tma_ok(p.k, k_st, s->d) &&
+                 tma_ok(p.v, v_st, s->dv);
   if (use_tma) {
     use_tma = encode_map(&maps[0], p.q, s->d, s->n_q, s->H, s->B, q_st, T::QP, T::TQ) &&
               encode_map(&maps[1], p.k, s->d, s->n_kv, s->H, s->B, k_st, T::QP, TK) &&
@@ -341,8 +370,10 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
   static const bool force_generic = std::getenv("ELSA_FORCE_GENERIC_LOAD") != nullptr;
   if (force_generic) use_tma = false;
 
-  auto kern = use_tma ? fwd_f32_kernel<W, TK, ST, R, true, D, DV>
-                      : fwd_f32_kernel<W, TK, ST, R, false, D, DV>;
+  auto kern = fwd_f32_kernel<W, TK, ST, R, false, D, DV>;
+  if constexpr (T::QP <= 256) {
+    if (use_tma) kern = fwd_f32_kernel<W, TK, ST, R, true, D, DV>;
+  }
   const int slot = cfg_slot * 2 + (use_tma ? 1 : 0);
   if (!dc->attr[slot]) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -385,6 +416,12 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
     case kCfgW8R8D96V128:
       return launch_fwd_cfg<8, 64, 2, 8, 96, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
                                                   kCfgW8R8D96V128, dc, stream);
+    case kCfgW4R8D256:
+      return launch_fwd_cfg<4, 32, 2, 8, 256>(p, s, q_st, k_st, v_st, splits, bh_count,
+                                              kCfgW4R8D256, dc, stream);
+    case kCfgW4R8D256V128:
+      return launch_fwd_cfg<4, 32, 2, 8, 256, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
+                                                   kCfgW4R8D256V128, dc, stream);
     default:
       return launch_fwd_cfg<4, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW4R8, dc,
                                          stream);

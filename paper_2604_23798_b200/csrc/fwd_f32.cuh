@@ -112,6 +112,7 @@ struct FwdParams {
   int pw_vec;           // float4 stores to pW legal
   int* err;
   unsigned long long* trace;  // ELSA_TRACE builds: per-warp phase timestamps
+  int q_vec, k_vec, v_vec;    // copy engine: 16-byte aligned rows (base and strides)
 };
 
 // Phase-timestamp instrumentation (compiled in only with -DELSA_TRACE): for
@@ -159,7 +160,7 @@ struct FwdTraits {
   static constexpr int R = R_;            // query rows per lane
   static constexpr int RP = R / 2;        // row pairs per lane
   static constexpr int WR = 2 * R;        // query rows per warp
-  static constexpr int D = D_;            // padded head width of Q/K: 64, 96 or 128
+  static constexpr int D = D_;            // padded head width of Q/K: 64, 96, 128 or 256
   static constexpr int DV = DV_;          // V columns per CTA (64 or 128); wider V runs as slices (grid z)
   static constexpr int CV = DV / 16;      // GEMM2 columns per lane: 4g + 64v + c, v < DV/64, c < 4
   static constexpr int NV4 = DV / 64;     // float4 V loads per key per lane
@@ -185,11 +186,18 @@ struct FwdTraits {
   // setmaxnreg can move registers from producers to consumers — the register
   // file is split per SM sub-partition (16K entries each, warps assigned
   // round-robin), so 9 warps would cap every warp at 168 registers.
-  // DV = 128: the 128-column W accumulator needs the same register split.
-  static constexpr bool kRegSplit = R >= 16 || DV > 64;
+  // DV = 128: the 128-column W accumulator needs the same register split
+  // (with 8 consumer warps; 4 consumer warps already launch at 255).
+  static constexpr bool kRegSplit = R >= 16 || (DV > 64 && W > 4);
   static constexpr int PRODUCER_WARPS = kRegSplit ? 4 : 1;
   static constexpr int THREADS = (W + PRODUCER_WARPS) * 32;
-  static constexpr int MIN_CTAS = (W <= 4 && R <= 8) ? 2 : 1;
+  // two CTAs per SM when a 4-warp CTA's shared memory leaves room for two
+  static constexpr int MIN_CTAS =
+      (W <= 4 && R <= 8 &&
+       2 * (size_t(D * TQ + STAGES * (TK * (D + 4) + TK * DV) + W * (TK / PH) * PTP) * 4 + 64) <=
+           227 * 1024)
+          ? 2
+          : 1;
   static constexpr int WARPS_PER_SMSP = (MIN_CTAS * (W + PRODUCER_WARPS) + 3) / 4;
   // launch-time register cap (per-SMSP file / warps resident on it, granule 8)
   static constexpr int MAX_REGS = (16384 / (WARPS_PER_SMSP * 32)) / 8 * 8 > 255
@@ -233,48 +241,59 @@ struct FwdTraits {
                 "TMA destinations must stay 128-byte aligned");
 };
 
+// Rows [0, ROWS) of PITCH floats into shared memory with cp.async (LDGSTS):
+// row r reads `width` floats at src + r * stride while r < valid_rows; the
+// rest of every row and the invalid rows are zero-filled. 16-byte copies when
+// `vec` (16-byte aligned rows), else 4-byte ones.
+template <int ROWS, int PITCH>
+__device__ __forceinline__ void async_rows(float* dst, const float* src, int64_t stride,
+                                           int valid_rows, int width, bool vec, int lane) {
+  static_assert(PITCH % 4 == 0, "16-byte chunks");
+  const uint32_t d0 = ptx::smem_u32(dst);
+  if (vec) {
+    constexpr int C4 = PITCH / 4;
+    for (int idx = lane; idx < ROWS * C4; idx += 32) {
+      const int r = idx / C4, c = (idx - r * C4) * 4;
+      const int n = (r < valid_rows && c < width) ? (width - c < 4 ? width - c : 4) : 0;
+      ptx::cp_async16(d0 + uint32_t(idx) * 16, n ? src + int64_t(r) * stride + c : src,
+                      uint32_t(n) * 4);
+    }
+  } else {
+    for (int idx = lane; idx < ROWS * PITCH; idx += 32) {
+      const int r = idx / PITCH, c = idx - r * PITCH;
+      const bool ok = r < valid_rows && c < width;
+      ptx::cp_async4(d0 + uint32_t(idx) * 4, ok ? src + int64_t(r) * stride + c : src,
+                     ok ? 4u : 0u);
+    }
+  }
+}
+
 template <class T>
 __device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw, float* Ks,
                                                  float* Vs, uint64_t* full, uint64_t* empty,
                                                  uint64_t* qbar, uint64_t* qfree, int b, int h,
                                                  int q0, int col0, int split_lo, int ntiles,
                                                  int lane) {
-  // Plain-load fallback for operands TMA cannot describe (misaligned base or
-  // strides, zero strides). Same smem layout as the TMA boxes, zero-filled.
-  const float* qg = p.q + int64_t(b) * p.qs_b + int64_t(h) * p.qs_h;
-  for (int idx = lane; idx < T::QRAW_FLOATS; idx += 32) {
-    const int r = idx / T::QP, c = idx - r * T::QP;
-    float val = 0.f;
-    if (c < p.d && q0 + r < p.n_q) val = qg[int64_t(q0 + r) * p.qs_r + c];
-    Qraw[idx] = val;
-  }
-  __threadfence_block();
-  __syncwarp();
-  if (lane == 0) ptx::mbar_arrive(qbar);
+  // Copy engine for operands TMA cannot describe (misaligned base or strides,
+  // zero strides, rows wider than a 256-element box): the whole producer warp
+  // issues asynchronous copies into the same smem layouts as the TMA boxes
+  // (zero-filled), and every lane's completion arrives on the stage barrier
+  // (count 32).
+  const float* qg = p.q + int64_t(b) * p.qs_b + int64_t(h) * p.qs_h + int64_t(q0) * p.qs_r;
+  async_rows<T::TQ, T::QP>(Qraw, qg, p.qs_r, p.n_q - q0, p.d, p.q_vec, lane);
+  ptx::cp_async_arrive(qbar);
   if constexpr (T::kQrawInK) ptx::mbar_wait(qfree, 0);  // raw Q sits in the K ring until transposed
   const float* kg = p.k + int64_t(b) * p.ks_b + int64_t(h) * p.ks_h;
-  const float* vg = p.v + int64_t(b) * p.vs_b + int64_t(h) * p.vs_h;
+  const float* vg = p.v + int64_t(b) * p.vs_b + int64_t(h) * p.vs_h + col0;
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % T::STAGES;
     if (t >= T::STAGES) ptx::mbar_wait_backoff(&empty[s], ((t / T::STAGES) - 1) & 1, ELSA_PRODUCER_SLEEP_NS);
     const int key0 = split_lo + t * T::TK;
-    float* ks = Ks + s * T::K_FLOATS;
-    float* vs = Vs + s * T::V_FLOATS;
-    for (int idx = lane; idx < T::K_FLOATS; idx += 32) {
-      const int r = idx / T::QP, c = idx - r * T::QP;
-      float val = 0.f;
-      if (c < p.d && key0 + r < p.n_kv) val = kg[int64_t(key0 + r) * p.ks_r + c];
-      ks[idx] = val;
-    }
-    for (int idx = lane; idx < T::V_FLOATS; idx += 32) {
-      const int r = idx / T::VP, c = idx - r * T::VP;
-      float val = 0.f;
-      if (col0 + c < p.dv && key0 + r < p.n_kv) val = vg[int64_t(key0 + r) * p.vs_r + col0 + c];
-      vs[idx] = val;
-    }
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&full[s]);
+    async_rows<T::TK, T::QP>(Ks + s * T::K_FLOATS, kg + int64_t(key0) * p.ks_r, p.ks_r,
+                             p.n_kv - key0, p.d, p.k_vec, lane);
+    async_rows<T::TK, T::VP>(Vs + s * T::V_FLOATS, vg + int64_t(key0) * p.vs_r, p.vs_r,
+                             p.n_kv - key0, p.dv - col0, p.v_vec, lane);
+    ptx::cp_async_arrive(&full[s]);
   }
 }
 
@@ -323,11 +342,12 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
 
   trace_cta(p, 0);
   if (threadIdx.x == 0) {
+    // TMA: one arrive.expect_tx per stage; copy engine: one arrival per lane
     for (int s = 0; s < T::STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], kTMA ? 1 : 32);
       ptx::mbar_init(&empty[s], T::W);
     }
-    ptx::mbar_init(qbar, 1);
+    ptx::mbar_init(qbar, kTMA ? 1 : 32);
     if constexpr (T::kQrawInK) ptx::mbar_init(qfree, T::W);
     ptx::fence_barrier_init();
   }

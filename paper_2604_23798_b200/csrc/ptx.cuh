@@ -108,6 +108,24 @@ __device__ __forceinline__ void sts128(uint32_t saddr, const uint4& v) {
                : "memory");
 }
 
+// Asynchronous global -> shared copies (LDGSTS): `bytes` of the cp-size are
+// read from `src`, the rest of the destination is zero-filled (bytes = 0:
+// nothing is read). Completion is tracked by cp_async_arrive on an mbarrier.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes)
+               : "memory");
+}
+// this thread's arrival on `bar` fires once all its prior cp.async copies have
+// landed (the barrier counts one arrival per thread)
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
 __device__ __forceinline__ float4 lds128(const float* p) {
   return *reinterpret_cast<const float4*>(p);
 }

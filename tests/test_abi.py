@@ -83,7 +83,7 @@ def test_split_planner():
 
 
 @pytest.mark.parametrize("bad", [
-    dict(d=129), dict(dv=4097), dict(dv=0), dict(d=0), dict(n_kv=0),
+    dict(d=257), dict(dv=4097), dict(dv=0), dict(d=0), dict(n_kv=0),
 ])
 def test_invalid_shapes_rejected_without_touching_the_gpu(bad):
     kw = dict(B=1, H=1, n_q=8, n_kv=8, d=64, dv=64)

@@ -312,8 +312,8 @@ def test_rejects_unsupported_inputs_on_gpu():
     with pytest.raises(elsa.ShapeError):
         elsa.scaled_dot_product_attention(q.double(), q.double(), q.double())
     with pytest.raises(elsa.ShapeError):
-        elsa.scaled_dot_product_attention(torch.randn(1, 1, 8, 129, device=DEV),
-                                          torch.randn(1, 1, 8, 129, device=DEV), q)
+        elsa.scaled_dot_product_attention(torch.randn(1, 1, 8, 257, device=DEV),
+                                          torch.randn(1, 1, 8, 257, device=DEV), q)
 
 
 # ---------------------------------------------------------------- reference-facing shim

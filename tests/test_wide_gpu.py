@@ -1,5 +1,5 @@
-"""Wide heads on the FP32 path: Q/K up to 128 floats (the w8r8d96 / w8r8d128
-kernels, raw Q staged in the K ring) and V of any width as 64-column slices (grid z),
+"""Wide heads on the FP32 path: Q/K up to 256 floats (the w8r8d96 / w8r8d128 /
+w4r8d256 kernels, raw Q staged in the K ring) and V of any width as 64-column slices (grid z),
 through every entry that carries V columns — the forward (single launch and
 kv splits + K2 merge), partial states, merge_states, the peer merge,
 blockwise states + the block combine, and the host-buffer entry. The
@@ -44,7 +44,8 @@ def _bound(y, ref, n, what):
 
 @pytest.mark.parametrize("d,dv", [
     (128, 128), (128, 64), (64, 128), (96, 96), (80, 200), (65, 65), (127, 1), (100, 130),
-    (128, 256), (16, 192), (128, 8), (96, 64), (88, 40), (72, 128)])
+    (128, 256), (16, 192), (128, 8), (96, 64), (88, 40), (72, 128), (256, 256), (192, 64),
+    (200, 130), (129, 1), (256, 40)])
 @pytest.mark.parametrize("splits", [1, 3])
 def test_wide_heads_vs_fp64(d, dv, splits):
     n = 333
@@ -176,7 +177,7 @@ def test_wide_host_entry_matches_device_bitwise():
 
 
 def test_too_wide_rejected():
-    q = torch.randn(1, 1, 8, 129, device=DEV)
+    q = torch.randn(1, 1, 8, 257, device=DEV)
     v = torch.randn(1, 1, 8, 64, device=DEV)
     with pytest.raises(elsa.ShapeError):
         elsa.scaled_dot_product_attention(q, q, v)

@@ -37,7 +37,8 @@ def timeit(fn):
     return ts[len(ts) // 2]
 
 
-for d, dv in ((64, 64), (128, 128), (128, 64), (64, 128), (96, 96), (80, 80), (128, 256)):
+for d, dv in ((64, 64), (128, 128), (128, 64), (64, 128), (96, 96), (80, 80), (128, 256),
+              (256, 256), (256, 64), (192, 192)):
     torch.manual_seed(0)
     q = torch.randn(1, H, n, d, device=dev)
     k = torch.randn(1, H, n, d, device=dev)
