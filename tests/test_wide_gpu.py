@@ -183,3 +183,35 @@ def test_too_wide_rejected():
         elsa.scaled_dot_product_attention(q, q, v)
     with pytest.raises(elsa.ShapeError):
         elsa.scaled_dot_product_attention(v, v, torch.randn(1, 1, 8, 4097, device=DEV))
+
+
+_COPY_ENGINE_CHILD = r"""
+import os, sys, numpy as np, torch
+sys.path.insert(0, os.environ["ELSA_REPO"])
+import paper_2604_23798_b200 as elsa
+out = {}
+for i, (n, d, dv) in enumerate(((300, 64, 64), (257, 96, 130), (200, 128, 128), (150, 256, 72))):
+    g = torch.Generator().manual_seed(i)
+    q, k, v = (torch.randn(1, 2, n, w, generator=g).cuda() for w in (d, d, dv))
+    out[f"y{i}"] = elsa.scaled_dot_product_attention(q, k, v).cpu().numpy()
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_copy_engine_bitwise_equals_tma(tmp_path):
+    # the copy engine (forced for every operand) fills the same shared-memory
+    # layouts as TMA, so Y must be bitwise identical to the TMA path's
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "ce.npz"
+    env = dict(os.environ, ELSA_FORCE_GENERIC_LOAD="1", ELSA_REPO=repo)
+    subprocess.run([sys.executable, "-c", _COPY_ENGINE_CHILD, str(out)], env=env, check=True,
+                   timeout=300)
+    ce = np.load(out)
+    for i, (n, d, dv) in enumerate(((300, 64, 64), (257, 96, 130), (200, 128, 128), (150, 256, 72))):
+        g = torch.Generator().manual_seed(i)
+        q, k, v = (torch.randn(1, 2, n, w, generator=g).to(DEV) for w in (d, d, dv))
+        y = elsa.scaled_dot_product_attention(q, k, v).cpu().numpy()
+        assert np.array_equal(y, ce[f"y{i}"]), (n, d, dv)
