@@ -481,7 +481,8 @@ void fill_common(FwdParams& p, const float* q, const float* k, const float* v,
 size_t split_ws_bytes(const elsa_shape* s, const Plan& pl) {
   if (pl.splits <= 1) return 0;
   const size_t rows = size_t(pl.heads_per_batch) * size_t(s->n_q);
-  return size_t(pl.splits) * rows * size_t(2 + 64 * dv_slices(s->dv)) * sizeof(float);
+  // m | S | (pad to 16 bytes) | W
+  return size_t(pl.splits) * rows * size_t(2 + 64 * dv_slices(s->dv)) * sizeof(float) + 16;
 }
 
 bool encode_map16(CUtensorMap* map, const void* base, int64_t rows, int64_t H, int64_t B,
@@ -567,10 +568,11 @@ int run_forward(const float* q, const float* k, const float* v, const elsa_shape
     p.mode = kModePartialLog2;
     p.pm = ws;
     p.pS = ws + int64_t(splits) * rows;
-    p.pW = ws + int64_t(splits) * rows * 2;
+    // W starts on a 16-byte boundary (float4 stores); the pitch is a multiple of 4
+    p.pW = ws + ((int64_t(splits) * rows * 2 + 3) & ~int64_t(3));
     p.part_stride = rows;
     p.pw_pitch = int(64 * dv_slices(shp->dv));
-    p.pw_vec = 1;
+    p.pw_vec = reinterpret_cast<uintptr_t>(p.pW) % 16 == 0;
     if (int st = launch_fwd(p, shp, q_st, k_st, v_st, plan, cnt, dc, strm)) return st;
     MergeParams mp;
     std::memset(&mp, 0, sizeof(mp));

@@ -79,7 +79,7 @@ def test_split_planner():
     assert resolve(_shape(1, 1, 64, 64 * 10), 4) == 4
     assert resolve(_shape(1, 1, 64, 64 * 10), 7) == 5
     ws = _lib.lib().elsa_workspace_bytes(ctypes.byref(_shape(1, 1, 1024, 1024)), 4)
-    assert ws == 4 * 1024 * 66 * 4
+    assert ws == 4 * 1024 * 66 * 4 + 16  # m | S | 16-byte pad | W
 
 
 @pytest.mark.parametrize("bad", [
@@ -124,7 +124,7 @@ def test_wide_head_workspace_counts_every_column_slice():
     h = _lib.lib()
     for d, dv, per_row in ((128, 64, 66), (64, 128, 130), (128, 200, 2 + 256), (96, 1, 66)):
         ws = h.elsa_workspace_bytes(ctypes.byref(_shape(1, 1, 1024, 1024, d=d, dv=dv)), 4)
-        assert ws == 4 * 1024 * per_row * 4, (d, dv, ws)
+        assert ws == 4 * 1024 * per_row * 4 + 16, (d, dv, ws)
     assert h.elsa_block_scan_workspace_bytes(10, 5, 200) == 10 * 8 * 202 * 4
     assert h.elsa_block_scan_workspace_bytes(10, 5, 4097) == 0
 

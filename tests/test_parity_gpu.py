@@ -401,3 +401,16 @@ def test_unusual_geometries(B, H, n_q, n_kv):
         return
     ref = oracle.naive_attention_rows_fp64(Q, K, V)
     assert_bound(y, ref, n_kv, f"{B}x{H}x{n_q}x{n_kv}")
+
+
+@pytest.mark.parametrize("n_q,n_kv,splits", [(233, 180, 3), (1, 700, 5), (77, 1000, 7)])
+def test_split_workspace_alignment_odd_rows(n_q, n_kv, splits):
+    # odd (rows x splits): the split workspace's W block must still start on a
+    # 16-byte boundary for the float4 partial-state stores (regression: it
+    # followed m | S directly and faulted)
+    rng = np.random.default_rng(n_q * 7 + splits)
+    Q = rng.standard_normal((1, 3, n_q, 64)).astype(np.float32)
+    K = rng.standard_normal((1, 3, n_kv, 64)).astype(np.float32)
+    V = rng.standard_normal((1, 3, n_kv, 64)).astype(np.float32)
+    y = run(Q, K, V, kv_splits=splits)
+    assert_bound(y, oracle.naive_attention(Q, K, V), n_kv, f"{n_q}x{n_kv}/{splits}")

@@ -215,3 +215,30 @@ def test_copy_engine_bitwise_equals_tma(tmp_path):
         q, k, v = (torch.randn(1, 2, n, w, generator=g).to(DEV) for w in (d, d, dv))
         y = elsa.scaled_dot_product_attention(q, k, v).cpu().numpy()
         assert np.array_equal(y, ce[f"y{i}"]), (n, d, dv)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_geometry_fuzz(seed):
+    # seeded random shapes / widths / views / splits / scales against FP64
+    rng = np.random.default_rng(1000 + seed)
+    B, H = int(rng.integers(1, 3)), int(rng.integers(1, 4))
+    n_q, n_kv = int(rng.integers(1, 400)), int(rng.integers(1, 700))
+    d, dv = int(rng.integers(1, 257)), int(rng.integers(1, 300))
+    pad = int(rng.integers(0, 3)) * 4            # row padding (keeps 16-byte rows when 0 or 4k)
+    off = int(rng.integers(0, 2))                # 4-byte base offset -> copy engine
+    splits = int(rng.choice([0, 1, 2, 5]))
+    scale = None if rng.random() < 0.5 else float(rng.uniform(-0.3, 0.3))
+
+    def make(n, w):
+        base = torch.from_numpy(rng.standard_normal(B * H * n * (w + pad) + off)
+                                .astype(np.float32)).to(DEV)
+        return base[off:].view(B, H, n, w + pad)[..., :w]
+
+    q, k, v = make(n_q, d), make(n_kv, d), make(n_kv, dv)
+    y = elsa.scaled_dot_product_attention(q, k, v, scale=scale, kv_splits=splits,
+                                          check_numerics=True).cpu().numpy()
+    Q, K, V = (t.cpu().numpy() for t in (q, k, v))
+    ref = oracle.naive_attention(Q, K, V, scale=scale)
+    err = oracle.row_err_conditioned(y, Q, K, V, ref=ref, scale=scale)
+    thr = oracle.bound_threshold(n_kv)
+    assert err.max() <= thr, (B, H, n_q, n_kv, d, dv, pad, off, splits, scale, err.max())
