@@ -242,3 +242,30 @@ def test_random_geometry_fuzz(seed):
     err = oracle.row_err_conditioned(y, Q, K, V, ref=ref, scale=scale)
     thr = oracle.bound_threshold(n_kv)
     assert err.max() <= thr, (B, H, n_q, n_kv, d, dv, pad, off, splits, scale, err.max())
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_partial_states_and_host_fuzz(seed):
+    # partial states over random key ranges / split counts vs FP64, and the
+    # host-buffer entry vs the device entry (bitwise) on random geometries
+    rng = np.random.default_rng(5000 + seed)
+    B, H = int(rng.integers(1, 3)), int(rng.integers(1, 4))
+    n_q, n_kv = int(rng.integers(1, 300)), int(rng.integers(2, 600))
+    d, dv = int(rng.integers(1, 257)), int(rng.integers(1, 200))
+    Q, K, V = _inputs(seed, B, H, n_q, n_kv, d, dv)
+    q, k, v = gpu(Q), gpu(K), gpu(V)
+    lo = int(rng.integers(0, n_kv - 1))
+    hi = int(rng.integers(lo + 1, n_kv + 1))
+    splits = int(rng.choice([0, 1, 2, 3, 8]))
+    m, S, W = (t.cpu().numpy() for t in elsa.partial_states(q, k, v, lo, hi, kv_splits=splits))
+    m64, S64, W64 = oracle.partial_state_fp64(Q, K, V, lo, hi)
+    np.testing.assert_allclose(m, m64, rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(S, S64 * np.exp(m64 - m.astype(np.float64)), rtol=2e-4)
+    y = W / S[..., None]
+    y64 = W64 / S64[..., None]
+    mag = np.linalg.norm(np.abs(W64) / S64[..., None], axis=-1)
+    err = np.linalg.norm(y - y64, axis=-1) / np.maximum(mag, 1e-300)
+    assert err.max() <= oracle.bound_threshold(hi - lo), err.max()
+    yh = elsa.attention_from_host(torch.from_numpy(Q), torch.from_numpy(K), torch.from_numpy(V))
+    yd = elsa.scaled_dot_product_attention(q, k, v).cpu()
+    assert torch.equal(yh, yd)
