@@ -67,3 +67,25 @@ def test_query_sharded_control_matches_direct(pg, B, H, n):
     q, k, v = (torch.randn(B, H, n, 64, device=DEV, generator=g) for _ in range(3))
     y = edist.query_sharded_attention(q, k, v, gather=True)
     assert torch.equal(y, elsa.scaled_dot_product_attention(q, k, v))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_kv_sharded_fuzz_widths_and_chunks(pg, seed):
+    # random n_q != n_kv, head widths and chunk counts through both exchanges
+    rng = np.random.default_rng(9000 + seed)
+    B, H = int(rng.integers(1, 3)), int(rng.integers(1, 4))
+    n_q, n = int(rng.integers(1, 400)), int(rng.integers(8, 900))
+    d, dv = int(rng.integers(1, 200)), int(rng.integers(1, 200))
+    chunks = int(rng.choice([1, 2, 3, 5, 8]))
+    Q = rng.standard_normal((B, H, n_q, d)).astype(np.float32)
+    K = rng.standard_normal((B, H, n, d)).astype(np.float32)
+    V = rng.standard_normal((B, H, n, dv)).astype(np.float32)
+    q, k, v = (torch.from_numpy(x).to(DEV) for x in (Q, K, V))
+    kl, vl, off = edist.shard_kv(k, v, 0, 1, chunks)
+    y_nccl = edist.kv_sharded_attention(q, kl, vl, off, n, chunks=chunks, exchange="nccl")
+    y_peer = edist.kv_sharded_attention(q, kl, vl, off, n, chunks=chunks, exchange="peer")
+    elsa.check_device_error(DEV)
+    assert torch.equal(y_nccl, y_peer)
+    ref = oracle.naive_attention(Q, K, V)
+    err = oracle.row_err_conditioned(y_peer.cpu().numpy(), Q, K, V, ref=ref)
+    assert err.max() <= oracle.bound_threshold(n), err.max()

@@ -269,3 +269,27 @@ def test_random_partial_states_and_host_fuzz(seed):
     yh = elsa.attention_from_host(torch.from_numpy(Q), torch.from_numpy(K), torch.from_numpy(V))
     yd = elsa.scaled_dot_product_attention(q, k, v).cpu()
     assert torch.equal(yh, yd)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_blockwise_fuzz(seed):
+    # per-block states for random block sizes / widths, their combine, and the
+    # exclusive prefixes, against FP64
+    rng = np.random.default_rng(11000 + seed)
+    B, H = int(rng.integers(1, 3)), int(rng.integers(1, 3))
+    n_q, n_kv = int(rng.integers(1, 120)), int(rng.integers(1, 700))
+    d, dv = int(rng.integers(1, 257)), int(rng.integers(1, 160))
+    bs = int(rng.choice([1, 7, 32, 64, 100, 128, 1000]))
+    Q, K, V = _inputs(seed + 50, B, H, n_q, n_kv, d, dv)
+    q, k, v = gpu(Q), gpu(K), gpu(V)
+    m, S, W = elsa.blockwise_states(q, k, v, block_size=bs)
+    nb = -(-n_kv // bs)
+    assert W.shape == (B, H, n_q, nb, dv)
+    m64, S64, W64 = oracle.blockwise_states_fp64(Q, K, V, bs)
+    assert np.array_equal(np.isneginf(m.cpu().numpy()), np.isneginf(m64))
+    (tm, tS, tW), (pm, pS, pW) = elsa.inter_block_combine(m, S, W, return_prefixes=True)
+    y = (tW / tS[..., None]).cpu().numpy()
+    ref = oracle.naive_attention(Q, K, V)
+    err = oracle.row_err_conditioned(y, Q, K, V, ref=ref)
+    assert err.max() <= oracle.bound_threshold(n_kv), err.max()
+    assert torch.all(torch.isneginf(pm[..., 0])) and torch.all(pS[..., 0] == 0)
