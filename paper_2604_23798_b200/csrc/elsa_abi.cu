@@ -110,9 +110,10 @@ int current_device_cache(DeviceCache** out) {
 //   w8r8d128: w8r8 with Q/K 128 floats wide (64 < d <= 128; Q^T and the K
 //          ring fill 200 KB, raw Q is staged in the K ring)
 //   w8r8d96, w8r8d96v128: the same with Q/K 96 wide (64 < d <= 96)
-//   w4r8d256, w4r8d256v128: 128 < d <= 256: 4 consumer warps x 16 rows
-//          (TQ = 64), 32-key tiles, plain loads (TMA boxes stop at 256
-//          elements, the padded pitch is 260), 1 CTA / SM
+//   w8r8d256 (dv <= 64), w4r8d256v128: 128 < d <= 256: 8 (4) consumer warps
+//          x 16 rows, 32-key tiles, the copy engine (TMA boxes stop at 256
+//          elements, the padded pitch is 260; w8r8d256 copies Q straight into
+//          Q^T and passes P in two halves to fit 227 KB), 1 CTA / SM
 //   w8r8v128, w8r8d128v128: 128 V columns per CTA (dv > 64): a 128-column
 //          W accumulator (setmaxnreg register split with a producer
 //          warpgroup); with d > 64 too, P^T goes through shared memory in
@@ -130,7 +131,7 @@ enum CfgId {
   kCfgW8R8D128V128 = 5,
   kCfgW8R8D96 = 6,  // 64 < d <= 96: Q/K 96 wide (GEMM1 3/4 of the d = 128 kernel's)
   kCfgW8R8D96V128 = 7,
-  kCfgW4R8D256 = 8,  // 128 < d <= 256: 4 consumer warps, 32-key tiles, plain loads
+  kCfgW8R8D256 = 8,  // 128 < d <= 256, dv <= 64: 8 consumer warps, 32-key tiles, copy engine
   kCfgW4R8D256V128 = 9,
   kCfgAuto = -1
 };
@@ -146,7 +147,7 @@ int wide_cfg(int64_t d, int64_t dv) {
   if (d <= 64) return v ? int(kCfgW8R8V128) : -1;
   if (d <= 96) return v ? int(kCfgW8R8D96V128) : int(kCfgW8R8D96);
   if (d <= 128) return v ? int(kCfgW8R8D128V128) : int(kCfgW8R8D128);
-  return v ? int(kCfgW4R8D256V128) : int(kCfgW4R8D256);
+  return v ? int(kCfgW4R8D256V128) : int(kCfgW8R8D256);
 }
 constexpr int64_t kMaxD = 256;
 constexpr int64_t kMaxDv = 4096;
@@ -191,8 +192,8 @@ CfgInfo cfg_info(int cfg) {
       return {128, 64, 1, 6.7, 5.2};
     case kCfgW8R8D96V128:
       return {128, 64, 1, 9.4, 7.2};
-    case kCfgW4R8D256:  // 64 x 32 tiles
-      return {64, 32, 1, 4.0, 4.0};
+    case kCfgW8R8D256:  // 128 x 32 tiles
+      return {128, 32, 1, 8.0, 6.0};
     case kCfgW4R8D256V128:
       return {64, 32, 1, 5.0, 4.0};
     default:
@@ -416,9 +417,9 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
     case kCfgW8R8D96V128:
       return launch_fwd_cfg<8, 64, 2, 8, 96, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
                                                   kCfgW8R8D96V128, dc, stream);
-    case kCfgW4R8D256:
-      return launch_fwd_cfg<4, 32, 2, 8, 256>(p, s, q_st, k_st, v_st, splits, bh_count,
-                                              kCfgW4R8D256, dc, stream);
+    case kCfgW8R8D256:
+      return launch_fwd_cfg<8, 32, 2, 8, 256>(p, s, q_st, k_st, v_st, splits, bh_count,
+                                              kCfgW8R8D256, dc, stream);
     case kCfgW4R8D256V128:
       return launch_fwd_cfg<4, 32, 2, 8, 256, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
                                                    kCfgW4R8D256V128, dc, stream);

@@ -222,7 +222,10 @@ struct FwdTraits {
   // Where the raw Q box lands before the transpose: the P area when it fits
   // (d <= 64); for the wide-Q kernels the K ring (the producer then waits on a
   // "Q consumed" barrier before its first K/V load).
-  static constexpr bool kQrawInK = QRAW_FLOATS > P_FLOATS;
+  // If it fits neither (d = 256 with 128-row tiles), the copy engine writes Q
+  // straight into Q^T (kQtDirect; no TMA for such kernels).
+  static constexpr bool kQtDirect = QRAW_FLOATS > P_FLOATS && QRAW_FLOATS > STAGES * K_FLOATS;
+  static constexpr bool kQrawInK = QRAW_FLOATS > P_FLOATS && !kQtDirect;
   static constexpr size_t BAR_OFFSET =
       size_t(QT_FLOATS + STAGES * (K_FLOATS + V_FLOATS) + P_FLOATS) * 4;
   static constexpr size_t SMEM_BYTES = BAR_OFFSET + (2 * STAGES + 2) * 8;
@@ -233,8 +236,7 @@ struct FwdTraits {
   static_assert(DV == 64 || DV == 128, "V slice width");
   static_assert(RK % PH == 0, "P halves split the lane's GEMM1 keys evenly");
   static_assert(TQ <= 256, "TMA box rows <= 256");
-  static_assert(QRAW_FLOATS <= P_FLOATS || QRAW_FLOATS <= STAGES * K_FLOATS,
-                "raw Q must fit the P area or the K ring");
+  static_assert(!kQtDirect || QP > 256, "direct Q^T copies only in copy-engine-only kernels");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert((QT_FLOATS * 4) % 128 == 0 && (K_FLOATS * 4) % 128 == 0 &&
                     (V_FLOATS * 4) % 128 == 0,
@@ -269,7 +271,8 @@ __device__ __forceinline__ void async_rows(float* dst, const float* src, int64_t
 }
 
 template <class T>
-__device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw, float* Ks,
+__device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw, float* Qt,
+                                                 float* Ks,
                                                  float* Vs, uint64_t* full, uint64_t* empty,
                                                  uint64_t* qbar, uint64_t* qfree, int b, int h,
                                                  int q0, int col0, int split_lo, int ntiles,
@@ -280,7 +283,21 @@ __device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw
   // (zero-filled), and every lane's completion arrives on the stage barrier
   // (count 32).
   const float* qg = p.q + int64_t(b) * p.qs_b + int64_t(h) * p.qs_h + int64_t(q0) * p.qs_r;
-  async_rows<T::TQ, T::QP>(Qraw, qg, p.qs_r, p.n_q - q0, p.d, p.q_vec, lane);
+  if constexpr (T::kQtDirect) {
+    // element (row rr, column c) straight to Q^T[c][pos(rr)] (4-byte copies,
+    // lanes over rows so the shared stores stay conflict-free; once per CTA)
+    const uint32_t qt0 = ptx::smem_u32(Qt);
+    const int valid = p.n_q - q0;
+    for (int idx = lane; idx < T::TQ * T::D; idx += 32) {
+      const int c = idx / T::TQ, rr = idx - c * T::TQ, r = rr % T::WR;
+      const int pos = rr - r + T::R * (r & 1) + (r >> 1);
+      const bool ok = rr < valid && c < p.d;
+      ptx::cp_async4(qt0 + uint32_t(c * T::QTP + pos) * 4, ok ? qg + int64_t(rr) * p.qs_r + c : qg,
+                     ok ? 4u : 0u);
+    }
+  } else {
+    async_rows<T::TQ, T::QP>(Qraw, qg, p.qs_r, p.n_q - q0, p.d, p.q_vec, lane);
+  }
   ptx::cp_async_arrive(qbar);
   if constexpr (T::kQrawInK) ptx::mbar_wait(qfree, 0);  // raw Q sits in the K ring until transposed
   const float* kg = p.k + int64_t(b) * p.ks_b + int64_t(h) * p.ks_h;
@@ -307,6 +324,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
                    const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV) {
   using T = FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>;
+  static_assert(!(kTMA && T::kQtDirect), "direct Q^T needs the copy engine");
   constexpr int TK = T::TK, QP = T::QP, QTP = T::QTP, VP = T::VP, PTP = T::PTP, RK = T::RK;
   constexpr int R = T::R, RP = T::RP, WR = T::WR;
   using ptx::f32x2;
@@ -377,8 +395,8 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
         }
       }
     } else {
-      producer_generic<T>(p, Qraw, Ks, Vs, full, empty, qbar, qfree, b, h, q0, col0, split_lo,
-                          ntiles, lane);
+      producer_generic<T>(p, Qraw, Qt, Ks, Vs, full, empty, qbar, qfree, b, h, q0, col0,
+                          split_lo, ntiles, lane);
     }
     return;
   }
@@ -395,7 +413,17 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   // so a lane's R rows (rg + 2i) are R consecutive floats (R/4 LDS.128 per d).
   // The sign of a negative scale is folded in here (x = (-q).k * |c|).
   ptx::mbar_wait(qbar, 0);
-  {
+  if constexpr (T::kQtDirect) {
+    // Q^T arrived directly; fold a negative scale's sign into this warp's rows
+    if (p.neg) {
+      for (int c = lane; c < T::D; c += 32) {
+        float* row = Qt + c * QTP + warp * WR;
+#pragma unroll
+        for (int u = 0; u < WR; ++u) row[u] = -row[u];
+      }
+    }
+    __syncwarp();
+  } else {
     const float sgn = p.neg ? -1.f : 1.f;
     constexpr int LPR = 32 / WR;         // lanes per row (2 for R = 8, 1 for R = 16)
     constexpr int DSPAN = T::D / LPR;    // d values per lane
@@ -412,7 +440,9 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
       dst[(4 * c + 3) * QTP] = v.w * sgn;
     }
   }
-  if constexpr (T::kQrawInK) {
+  if constexpr (T::kQtDirect) {
+    // nothing to hand back: raw Q never occupied the P area or the K ring
+  } else if constexpr (T::kQrawInK) {
     // raw Q occupies the K ring: hand it back to the producer
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(qfree);
