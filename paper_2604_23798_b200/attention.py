@@ -329,10 +329,22 @@ def _sdpa_tc(q, k, v, sc, out):
     and FP32 (m, S, W) state; output in the input format)."""
     B, H, n_q, d = q.shape
     dv = v.shape[-1]
-    if d != 64 or dv != 64:
-        raise ShapeError(f"the 16-bit tensor-core path needs d = dv = 64, got d={d}, dv={dv}")
-    q, k, v = (t if t.stride(-1) == 1 and t.data_ptr() % 16 == 0 and all(
-        (s * 2) % 16 == 0 for s in t.stride()[:3]) else t.contiguous() for t in (q, k, v))
+    if d > 64 or dv > 64:
+        raise ShapeError(f"the 16-bit tensor-core path takes d, dv <= 64, got d={d}, dv={dv}")
+
+    def tma_ready(t):
+        # TMA operands: 16-byte aligned base and row strides. Otherwise copy
+        # into a buffer whose rows are padded to a multiple of 8 elements
+        # (the kernel reads the first d columns; TMA zero-fills the box).
+        if t.stride(-1) == 1 and t.data_ptr() % 16 == 0 and all(
+                (s * 2) % 16 == 0 for s in t.stride()[:3]):
+            return t
+        w = t.shape[-1]
+        buf = torch.empty((*t.shape[:-1], -(-w // 8) * 8), device=t.device, dtype=t.dtype)
+        buf[..., :w] = t
+        return buf[..., :w]
+
+    q, k, v = (tma_ready(t) for t in (q, k, v))
     if out is None:
         y = torch.empty((B, H, n_q, dv), device=q.device, dtype=q.dtype)
     else:

@@ -486,11 +486,13 @@ size_t split_ws_bytes(const elsa_shape* s, const Plan& pl) {
   return size_t(pl.splits) * rows * size_t(2 + 64 * dv_slices(s->dv)) * sizeof(float) + 16;
 }
 
-bool encode_map16(CUtensorMap* map, const void* base, int64_t rows, int64_t H, int64_t B,
+bool encode_map16(CUtensorMap* map, const void* base, int64_t inner, int64_t rows, int64_t H,
+                  int64_t B,
                   const int64_t st[3], bool bf16) {
   auto enc = encoder();
   if (!enc) return false;
-  cuuint64_t dims[4] = {64, cuuint64_t(rows), cuuint64_t(H), cuuint64_t(B)};
+  // inner < 64: the 64-wide box is zero-filled past the row (OOB fill)
+  cuuint64_t dims[4] = {cuuint64_t(inner), cuuint64_t(rows), cuuint64_t(H), cuuint64_t(B)};
   cuuint64_t strides[3] = {cuuint64_t(st[2] * 2), cuuint64_t(st[1] * 2), cuuint64_t(st[0] * 2)};
   cuuint32_t box[4] = {64, 128, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
@@ -886,7 +888,7 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
                  double scale, int is_bf16, void* stream) {
   t_last_launches = 0;
   if (!valid_shape(shp) || !std::isfinite(scale)) return ELSA_ERR_SHAPE;
-  if (shp->d != 64 || shp->dv != 64) return ELSA_ERR_SHAPE;
+  if (shp->d > 64 || shp->dv > 64) return ELSA_ERR_SHAPE;
   if (!q || !k || !v || !y) return ELSA_ERR_SHAPE;
   if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
   DeviceCache* dc = nullptr;
@@ -896,17 +898,20 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
   std::memcpy(k_st, shp->k_stride, sizeof(k_st));
   std::memcpy(v_st, shp->v_stride, sizeof(v_st));
   std::memcpy(y_st, shp->y_stride, sizeof(y_st));
-  sanitize(q_st, shp->n_q, shp->H, shp->B, 64);
-  sanitize(k_st, shp->n_kv, shp->H, shp->B, 64);
-  sanitize(v_st, shp->n_kv, shp->H, shp->B, 64);
-  sanitize(y_st, shp->n_q, shp->H, shp->B, 64);
-  if (!aligned16(q, q_st) || !aligned16(k, k_st) || !aligned16(v, v_st) || !aligned16(y, y_st))
-    return ELSA_ERR_SHAPE;
+  sanitize(q_st, shp->n_q, shp->H, shp->B, shp->d);
+  sanitize(k_st, shp->n_kv, shp->H, shp->B, shp->d);
+  sanitize(v_st, shp->n_kv, shp->H, shp->B, shp->dv);
+  sanitize(y_st, shp->n_q, shp->H, shp->B, shp->dv);
+  // Q, K, V go through TMA (16-byte aligned bases and row strides); Y may be
+  // stored element-wise
+  if (!aligned16(q, q_st) || !aligned16(k, k_st) || !aligned16(v, v_st)) return ELSA_ERR_SHAPE;
+  for (int i = 0; i < 3; ++i)
+    if (y_st[i] < 0) return ELSA_ERR_SHAPE;
   const bool bf16 = is_bf16 != 0;
   CUtensorMap maps[3];
-  if (!encode_map16(&maps[0], q, shp->n_q, shp->H, shp->B, q_st, bf16) ||
-      !encode_map16(&maps[1], k, shp->n_kv, shp->H, shp->B, k_st, bf16) ||
-      !encode_map16(&maps[2], v, shp->n_kv, shp->H, shp->B, v_st, bf16))
+  if (!encode_map16(&maps[0], q, shp->d, shp->n_q, shp->H, shp->B, q_st, bf16) ||
+      !encode_map16(&maps[1], k, shp->d, shp->n_kv, shp->H, shp->B, k_st, bf16) ||
+      !encode_map16(&maps[2], v, shp->dv, shp->n_kv, shp->H, shp->B, v_st, bf16))
     return ELSA_ERR_SHAPE;
   TcParams p;
   std::memset(&p, 0, sizeof(p));
@@ -915,6 +920,8 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
   p.H = int(shp->H);
   p.n_q = int(shp->n_q);
   p.n_kv = int(shp->n_kv);
+  p.dv = int(shp->dv);
+  p.y_vec = aligned16(y, y_st) ? 1 : 0;
   p.ys_b = y_st[0];
   p.ys_h = y_st[1];
   p.ys_r = y_st[2];

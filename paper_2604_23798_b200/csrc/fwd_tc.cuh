@@ -43,8 +43,10 @@
 namespace elsa {
 
 struct TcParams {
-  void* y;  // 16-bit output (B, H, n_q, 64) in the input format
+  void* y;  // 16-bit output (B, H, n_q, dv) in the input format
   int B, H, n_q, n_kv;
+  int dv;     // <= 64 (narrower Q/K/V are zero-filled to 64 by TMA)
+  int y_vec;  // 16-byte Y stores legal (else element stores)
   int64_t ys_b, ys_h, ys_r;  // element strides of y
   float c;                   // |scale| * log2(e)
   int neg;                   // scale < 0 (sign applied to the scores)
@@ -570,6 +572,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
                             2 * (int64_t(b) * p.ys_b + int64_t(h) * p.ys_h + int64_t(qrow) * p.ys_r);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
+        if (8 * u >= p.dv) break;
         uint4 pk;
         const float* x = w + 8 * u;
         if constexpr (kBF16) {
@@ -583,7 +586,16 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
           pk.z = tc::pack_f16x2(x[4] * inv, x[5] * inv);
           pk.w = tc::pack_f16x2(x[6] * inv, x[7] * inv);
         }
-        *reinterpret_cast<uint4*>(yrow + 16 * u) = pk;
+        if (p.y_vec && 8 * u + 8 <= p.dv) {
+          *reinterpret_cast<uint4*>(yrow + 16 * u) = pk;
+        } else {  // narrow / unaligned output rows: 16-bit element stores
+          const uint32_t wds[4] = {pk.x, pk.y, pk.z, pk.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (8 * u + e < p.dv)
+              reinterpret_cast<uint16_t*>(yrow)[8 * u + e] =
+                  uint16_t(e & 1 ? wds[e >> 1] >> 16 : wds[e >> 1] & 0xffffu);
+        }
       }
     }
   }

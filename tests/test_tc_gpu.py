@@ -21,14 +21,14 @@ import paper_2604_23798_b200 as elsa  # noqa: E402
 DEV = torch.device("cuda", 0)
 
 
-def _check(dtype, B, H, n_q, n_kv, seed, scale=None):
+def _check(dtype, B, H, n_q, n_kv, seed, scale=None, d=64, dv=64):
     g = torch.Generator(device=DEV)
     g.manual_seed(seed)
-    q = torch.randn(B, H, n_q, 64, device=DEV, generator=g).to(dtype)
-    k = torch.randn(B, H, n_kv, 64, device=DEV, generator=g).to(dtype)
-    v = torch.randn(B, H, n_kv, 64, device=DEV, generator=g).to(dtype)
+    q = torch.randn(B, H, n_q, d, device=DEV, generator=g).to(dtype)
+    k = torch.randn(B, H, n_kv, d, device=DEV, generator=g).to(dtype)
+    v = torch.randn(B, H, n_kv, dv, device=DEV, generator=g).to(dtype)
     y = elsa.scaled_dot_product_attention(q, k, v, scale=scale, check_numerics=True)
-    assert y.dtype == dtype and y.shape == (B, H, n_q, 64)
+    assert y.dtype == dtype and y.shape == (B, H, n_q, dv)
     ref = oracle.naive_attention(*(t.double().cpu().numpy() for t in (q, k, v)), scale=scale)
     ours = oracle.row_rel_err(y.double().cpu().numpy(), ref)
     # PyTorch's 16-bit SDPA returns NaN for a negative scale: give it the
@@ -59,9 +59,29 @@ def test_tc_negative_scale_and_determinism():
 
 
 def test_tc_rejects_other_head_dims():
-    q = torch.randn(1, 1, 16, 32, device=DEV, dtype=torch.bfloat16)
+    q = torch.randn(1, 1, 16, 96, device=DEV, dtype=torch.bfloat16)
     with pytest.raises(elsa.ShapeError):
         elsa.scaled_dot_product_attention(q, q, q)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("d,dv", [(32, 32), (16, 64), (64, 16), (40, 24), (8, 8), (60, 36),
+                                  (3, 5), (64, 1)])
+def test_tc_narrow_heads(dtype, d, dv):
+    # d, dv < 64: the 64-wide TMA boxes zero-fill past the row (rows not a
+    # multiple of 8 elements are first copied into padded rows); Y rows narrower
+    # than 64 are stored element-wise
+    if dv <= 8:  # narrow rows can cancel to ~0: absolute tolerance against FP32
+        g = torch.Generator(device=DEV)
+        g.manual_seed(d)
+        q, k = (torch.randn(1, 2, 300, d, device=DEV, generator=g).to(dtype) for _ in range(2))
+        v = torch.randn(1, 2, 300, dv, device=DEV, generator=g).to(dtype)
+        y = elsa.scaled_dot_product_attention(q, k, v, check_numerics=True)
+        ref = elsa.scaled_dot_product_attention(q.float(), k.float(), v.float())
+        assert y.shape == (1, 2, 300, dv)
+        assert torch.allclose(y.float(), ref, atol=2e-2, rtol=2e-2)
+        return
+    _check(dtype, 1, 3, 300, 333, seed=d * 100 + dv, d=d, dv=dv)
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
