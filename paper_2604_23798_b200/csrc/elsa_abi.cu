@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <string>
 #include <mutex>
 
 #include "elsa.h"
@@ -1241,10 +1242,16 @@ int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n
   int sms = 148;
   if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
   const Plan pl = plan_for(shp, shp->n_kv, kv_splits, sms);
-  static const char* names[] = {"w4r8", "w8r16", "w8r8"};
+  static const char* names[] = {"w4r8",     "w8r16",        "w8r8",    "w8r8d128",
+                                "w8r8v128", "w8r8d128v128", "w8r8d96", "w8r8d96v128",
+                                "w8r8d256", "w4r8d256v128"};
+  static_assert(sizeof(names) / sizeof(names[0]) == kCfgW4R8D256V128 + 1, "one name per config");
+  if (pl.cfg < 0 || pl.cfg > kCfgW4R8D256V128) return ELSA_ERR_SHAPE;
   const CfgInfo ci = cfg_info(pl.cfg);
-  std::snprintf(buf, n, "%s tq=%d tk=%d kv_splits=%d heads_per_batch=%lld", names[pl.cfg], ci.tq,
-                ci.tk, pl.splits, static_cast<long long>(pl.heads_per_batch));
+  const int64_t slices = ceil_div(shp->dv, cfg_dv(pl.cfg));
+  std::snprintf(buf, n, "%s tq=%d tk=%d kv_splits=%d heads_per_batch=%lld%s", names[pl.cfg],
+                ci.tq, ci.tk, pl.splits, static_cast<long long>(pl.heads_per_batch),
+                slices > 1 ? (" dv_slices=" + std::to_string(slices)).c_str() : "");
   return ELSA_OK;
 }
 

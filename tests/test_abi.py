@@ -162,3 +162,18 @@ def test_peer_merge_validates_before_touching_the_device():
     assert h.elsa_merge_peers_f32(arr, arr, arr, 0, 1, 4, 0, 4, 64, y, None) == 2
     assert h.elsa_merge_peers_f32(arr, arr, arr, 1, 8, 4, 2, 4, 64, y, None) == 2
     assert h.elsa_merge_peers_f32(None, arr, arr, 1, 8, 4, 0, 4, 64, y, None) == 2
+
+
+def test_describe_plan_names_every_width_configuration():
+    h = _lib.lib()
+    buf = ctypes.create_string_buffer(128)
+    want = {(64, 64): ("w8r8", "w4r8", "w8r16"), (128, 64): ("w8r8d128",), (64, 128): ("w8r8v128",),
+            (128, 128): ("w8r8d128v128",), (96, 96): ("w8r8d96v128",), (80, 40): ("w8r8d96",),
+            (256, 64): ("w8r8d256",), (200, 100): ("w4r8d256v128",)}
+    for (d, dv), names in want.items():
+        assert h.elsa_describe_plan(ctypes.byref(_shape(1, 16, 4096, 4096, d=d, dv=dv)), 0, buf,
+                                    128) == 0
+        desc = buf.value.decode()
+        assert desc.split()[0] in names, (d, dv, desc)
+    assert h.elsa_describe_plan(ctypes.byref(_shape(1, 1, 512, 512, d=128, dv=300)), 0, buf, 128) == 0
+    assert "dv_slices=3" in buf.value.decode()
