@@ -202,19 +202,20 @@ def depth_cap(n):
     return 2 * _clog2(n) + 3
 
 
-KEY_TILE = 64  # keys per tile in the forward kernel (FwdTraits::TK)
+KEY_TILE = 64  # keys per tile in the forward kernel (FwdTraits::TK; 32 for d > 128)
 
 
 def _precision_name(p):
     return getattr(p, "value", str(p)).lower()
 
 
-def analytic_trace(b, h, n, block_size, splits, workspace_bytes=None, d_v=64):
+def analytic_trace(b, h, n, block_size, splits, workspace_bytes=None, d_v=64,
+                   key_tile=KEY_TILE):
     """ScanTrace of the GPU schedule for a (b, h, n) problem run with
-    ``splits`` KV splits (see :class:`ScanTrace`); ``workspace_bytes`` is the
-    split workspace the library asked for (elsa_workspace_bytes), else the
-    unbatched size."""
-    tiles = -(-n // KEY_TILE)
+    ``splits`` KV splits and ``key_tile`` keys per tile (see
+    :class:`ScanTrace`); ``workspace_bytes`` is the split workspace the
+    library asked for (elsa_workspace_bytes), else the unbatched size."""
+    tiles = -(-n // key_tile)
     tps = -(-tiles // splits)
     paths = b * h * n
     return ScanTrace(
@@ -256,8 +257,10 @@ def scan_forward(problem, cfg=None, device=None):
     out = AttentionOutput(y_t4)
     trace = None
     if getattr(cfg, "trace", False):
+        plan = _att.describe_plan(q, k, v, splits_req)  # "<cfg> tq=.. tk=.. kv_splits=.."
+        tk = int(plan.split("tk=")[1].split()[0])
         trace = analytic_trace(b, h, n, cfg.block_size, resolve_kv_splits(q, k, v, splits_req),
-                               _att.workspace_bytes(q, k, v, splits_req))
+                               _att.workspace_bytes(q, k, v, splits_req), d_v=d_v, key_tile=tk)
     return out, trace
 
 
