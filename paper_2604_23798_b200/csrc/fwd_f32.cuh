@@ -161,9 +161,11 @@ struct FwdTraits {
   static constexpr int RP = R / 2;        // row pairs per lane
   static constexpr int WR = 2 * R;        // query rows per warp
   static constexpr int D = D_;            // padded head width of Q/K: 64, 96, 128 or 256
-  static constexpr int DV = DV_;          // V columns per CTA (64 or 128); wider V runs as slices (grid z)
-  static constexpr int CV = DV / 16;      // GEMM2 columns per lane: 4g + 64v + c, v < DV/64, c < 4
-  static constexpr int NV4 = DV / 64;     // float4 V loads per key per lane
+  static constexpr int DV = DV_;          // V columns per CTA (32, 64 or 128); wider V runs as slices (grid z)
+  static constexpr int CV = DV / 16;      // GEMM2 columns per lane: VW g + 16 VW v + c, v < NVL, c < VW
+  static constexpr int VW = DV >= 64 ? 4 : DV / 16;  // V floats per lane per load
+  static constexpr int NVL = DV / (16 * VW);          // V loads per key per lane
+  static constexpr int NV4 = VW == 4 ? NVL : 0;       // (float4 loads: the DV >= 64 kernels)
   static constexpr int TQ = WR * W;
   static constexpr int QP = D + 4;        // raw Q / K row pitch in floats (272 B; TMA box width)
   static constexpr int QTP = TQ;          // Q^T pitch: Qt[d][row position]
@@ -233,7 +235,7 @@ struct FwdTraits {
   static constexpr uint32_t Q_TX_BYTES = uint32_t(QRAW_FLOATS) * 4;
   static_assert(TK % 16 == 0, "TK must be a multiple of 16");
   static_assert(R % 4 == 0, "R must be a multiple of 4 (float4 row groups)");
-  static_assert(DV == 64 || DV == 128, "V slice width");
+  static_assert(DV == 32 || DV == 64 || DV == 128, "V slice width");
   static_assert(RK % PH == 0, "P halves split the lane's GEMM1 keys evenly");
   static_assert(TQ <= 256, "TMA box rows <= 256");
   static_assert(!kQtDirect || QP > 256, "direct Q^T copies only in copy-engine-only kernels");
@@ -460,7 +462,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   // Row pairs: lane rows (rg + 2i), i = 0..R-1, are held as R/2 packed pairs
   // ip = (i = 2ip, 2ip+1), so every GEMM FMA is an FFMA2 outer-product step.
   constexpr int CV = T::CV;
-  f32x2 o2[RP][CV];  // W accumulator: [row pair][column 4g + 64(c / 4) + c % 4]
+  f32x2 o2[RP][CV];  // W accumulator: [row pair][column VW g + 16 VW (c / VW) + c % VW]
   float mrow[R];    // running anchors (log2 units)
   f32x2 l2[RP];     // running normalizer partials (this lane's keys)
 #pragma unroll
@@ -477,19 +479,28 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   // P area (rows jj - k0)
   auto gemm2 = [&](int tt, int k0) {
     const int st = tt % T::STAGES;
-    const float* vs = Vs + st * T::V_FLOATS + 4 * g;
+    const float* vs = Vs + st * T::V_FLOATS + T::VW * g;
 #pragma unroll(T::G2_UNROLL)
     for (int jj = 0; jj < TK / T::PH; ++jj) {
       f32x2 pr[RP];
 #pragma unroll
       for (int u = 0; u < RP / 2; ++u)
         ptx::lds128x2(ptr + jj * PTP + 4 * u, pr[2 * u], pr[2 * u + 1]);
-      float4 vf[T::NV4];
+      float va[CV];
 #pragma unroll
-      for (int q = 0; q < T::NV4; ++q) vf[q] = ptx::lds128(vs + (k0 + jj) * VP + 64 * q);
+      for (int q = 0; q < T::NVL; ++q) {
+        const float* src = vs + (k0 + jj) * VP + 16 * T::VW * q;
+        if constexpr (T::VW == 4) {
+          const float4 f = ptx::lds128(src);
+          va[4 * q] = f.x, va[4 * q + 1] = f.y, va[4 * q + 2] = f.z, va[4 * q + 3] = f.w;
+        } else {
+          const float2 f = *reinterpret_cast<const float2*>(src);
+          va[2 * q] = f.x, va[2 * q + 1] = f.y;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < CV; ++c) {
-        const float vv = f4(vf[c / 4], c % 4);
+        const float vv = va[c];
         const f32x2 vb = ptx::pack2(vv, vv);
 #pragma unroll
         for (int u = 0; u < RP; ++u) {
@@ -692,14 +703,18 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
 #pragma unroll
         for (int c = 0; c < CV; ++c) yv[c] = __fdiv_rn(o[c], l);
 #pragma unroll
-        for (int v4 = 0; v4 < T::NV4; ++v4) {
-          const int col = col0 + 64 * v4 + 4 * g;
-          const float* yq = yv + 4 * v4;
-          if (p.y_vec && col + 3 < p.dv) {
-            *reinterpret_cast<float4*>(yrow + col) = make_float4(yq[0], yq[1], yq[2], yq[3]);
+        for (int v4 = 0; v4 < T::NVL; ++v4) {
+          constexpr int VW = T::VW;
+          const int col = col0 + 16 * VW * v4 + VW * g;
+          const float* yq = yv + VW * v4;
+          if (p.y_vec && col + VW - 1 < p.dv) {
+            if constexpr (VW == 4)
+              *reinterpret_cast<float4*>(yrow + col) = make_float4(yq[0], yq[1], yq[2], yq[3]);
+            else
+              *reinterpret_cast<float2*>(yrow + col) = make_float2(yq[0], yq[1]);
           } else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < VW; ++c)
               if (col + c < p.dv) yrow[col + c] = yq[c];
           }
         }
@@ -713,14 +728,18 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
         }
         float* wrow = p.pW + idx * p.pw_pitch;
 #pragma unroll
-        for (int v4 = 0; v4 < T::NV4; ++v4) {
-          const int col = col0 + 64 * v4 + 4 * g;
-          const float* oq = o + 4 * v4;
-          if (p.pw_vec && col + 3 < p.dv) {
-            *reinterpret_cast<float4*>(wrow + col) = make_float4(oq[0], oq[1], oq[2], oq[3]);
+        for (int v4 = 0; v4 < T::NVL; ++v4) {
+          constexpr int VW = T::VW;
+          const int col = col0 + 16 * VW * v4 + VW * g;
+          const float* oq = o + VW * v4;
+          if (p.pw_vec && col + VW - 1 < p.dv) {
+            if constexpr (VW == 4)
+              *reinterpret_cast<float4*>(wrow + col) = make_float4(oq[0], oq[1], oq[2], oq[3]);
+            else
+              *reinterpret_cast<float2*>(wrow + col) = make_float2(oq[0], oq[1]);
           } else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < VW; ++c)
               if (col + c < p.dv) wrow[col + c] = oq[c];
           }
         }

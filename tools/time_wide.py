@@ -3,7 +3,7 @@ B1 H16 n (default 16384) at (d, dv) in {64, 128}^2 plus a few odd widths.
 Rate = algorithmic 2 n^2 (d + dv) B H / t (the slices' recomputed scores are
 overhead, not counted). CUDA events, L2 flushed before every timed call.
 
-usage: python tools/time_wide.py [n] [reps]"""
+usage: python tools/time_wide.py [n] [reps] [d:dv,d:dv,...]"""
 import os
 import sys
 
@@ -37,8 +37,11 @@ def timeit(fn):
     return ts[len(ts) // 2]
 
 
-for d, dv in ((64, 64), (128, 128), (128, 64), (64, 128), (96, 96), (80, 80), (128, 256),
-              (256, 256), (256, 64), (192, 192)):
+PAIRS = ((64, 64), (128, 128), (128, 64), (64, 128), (96, 96), (80, 80), (128, 256),
+         (256, 256), (256, 64), (192, 192), (32, 32), (16, 16))
+if len(sys.argv) > 3:  # explicit "d:dv,d:dv,..."
+    PAIRS = tuple(tuple(int(x) for x in p.split(":")) for p in sys.argv[3].split(","))
+for d, dv in PAIRS:
     torch.manual_seed(0)
     q = torch.randn(1, H, n, d, device=dev)
     k = torch.randn(1, H, n, d, device=dev)
