@@ -89,3 +89,34 @@ def test_kv_sharded_fuzz_widths_and_chunks(pg, seed):
     ref = oracle.naive_attention(Q, K, V)
     err = oracle.row_err_conditioned(y_peer.cpu().numpy(), Q, K, V, ref=ref)
     assert err.max() <= oracle.bound_threshold(n), err.max()
+
+
+@pytest.mark.parametrize("ranks,per_rank,dv", [(2, 4, 64), (4, 2, 64), (8, 1, 64), (3, 2, 100),
+                                               (16, 2, 8)])
+def test_peer_merge_kernel_multi_rank_layout(ranks, per_rank, dv):
+    # the fused merge as a multi-GPU run drives it, simulated on one GPU: each
+    # "rank" owns per_rank consecutive chunks in its own buffer; every rank's
+    # row slice merged through the peer kernel must equal merge_states over
+    # all chunks in global order (rank-major, owned chunk minor), bitwise
+    rng = np.random.default_rng(ranks * 10 + per_rank)
+    chunks, rows = ranks * per_rank, 1000
+    m = rng.uniform(-5, 5, (chunks, rows)).astype(np.float32)
+    m[rng.random((chunks, rows)) < 0.05] = -np.inf
+    S = rng.uniform(0.5, 4, (chunks, rows)).astype(np.float32)
+    W = rng.standard_normal((chunks, rows, dv)).astype(np.float32)
+    S[np.isneginf(m)] = 0
+    W[np.isneginf(m)] = 0
+    S[:, 7] = np.maximum(S[:, 7], 0.5)  # keep at least one live chunk per row
+    m[0, :] = np.where(np.isneginf(m).all(axis=0), 0.0, m[0, :])
+    S[0, :] = np.where(S.sum(axis=0) == 0, 1.0, S[0, :])
+    mt, St, Wt = (torch.from_numpy(x).to(DEV) for x in (m, S, W))
+    want = elsa.merge_states(mt, St, Wt)
+    bufs = [(mt[r * per_rank:(r + 1) * per_rank].contiguous(),
+             St[r * per_rank:(r + 1) * per_rank].contiguous(),
+             Wt[r * per_rank:(r + 1) * per_rank].contiguous()) for r in range(ranks)]
+    mp = [b[0].data_ptr() for b in bufs]
+    Sp = [b[1].data_ptr() for b in bufs]
+    Wp = [b[2].data_ptr() for b in bufs]
+    for lo, hi in edist.row_slices(rows, ranks):
+        y = elsa.merge_peer_states(mp, Sp, Wp, per_rank, rows, lo, hi - lo, dv)
+        assert torch.equal(y, want[lo:hi]), (lo, hi)
