@@ -127,7 +127,7 @@ int elsa_partial_f32(const float* q, const float* k, const float* v,
 /* FP16 / BF16 variant: the QK^T and PV contractions on the
  * tcgen05 tensor cores with FP32 accumulation in TMEM; the (m, S, W) states,
  * their combine and the epilogue in FP32. q, k, v, y are 16-bit
- * (is_bf16 ? bfloat16 : float16) with d, dv <= 64; q, k, v with 16-byte
+ * (is_bf16 ? bfloat16 : float16) with d, dv <= 128; q, k, v with 16-byte
  * aligned bases and strides (TMA); y is written in the same format (any
  * strides). */
 int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y,

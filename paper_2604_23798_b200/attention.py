@@ -329,8 +329,8 @@ def _sdpa_tc(q, k, v, sc, out):
     and FP32 (m, S, W) state; output in the input format)."""
     B, H, n_q, d = q.shape
     dv = v.shape[-1]
-    if d > 64 or dv > 64:
-        raise ShapeError(f"the 16-bit tensor-core path takes d, dv <= 64, got d={d}, dv={dv}")
+    if d > 128 or dv > 128:
+        raise ShapeError(f"the 16-bit tensor-core path takes d, dv <= 128, got d={d}, dv={dv}")
 
     def tma_ready(t):
         # TMA operands: 16-byte aligned base and row strides. Otherwise copy

@@ -897,7 +897,8 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
                  double scale, int is_bf16, void* stream) {
   t_last_launches = 0;
   if (!valid_shape(shp) || !std::isfinite(scale)) return ELSA_ERR_SHAPE;
-  if (shp->d > 64 || shp->dv > 64) return ELSA_ERR_SHAPE;
+  if (shp->d > 128 || shp->dv > 128) return ELSA_ERR_SHAPE;
+  const bool wide16 = shp->d > 64 || shp->dv > 64;  // the D = 128 kernel (one query tile per CTA)
   if (!q || !k || !v || !y) return ELSA_ERR_SHAPE;
   if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
   DeviceCache* dc = nullptr;
@@ -948,6 +949,7 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
   const int64_t BH = shp->B * shp->H;
   int groups = ceil_div(shp->n_q, 256) * BH >= int64_t(dc->sms) ? 2 : 1;
   if (forced_groups == 1 || forced_groups == 2) groups = forced_groups;
+  if (wide16) groups = 1;
   auto launch = [&](auto traits, auto kern, int slot) -> int {
     using TT = decltype(traits);
     p.qtiles = int(ceil_div(shp->n_q, TT::ROWS));
@@ -963,9 +965,12 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
         p, maps[0], maps[1], maps[2]);
     return ELSA_OK;
   };
-  const int base = kAttrSlots - 4;  // the last four slots
+  const int base = kAttrSlots - 6;  // the last six slots
   int st;
-  if (groups == 2)
+  if (wide16)
+    st = bf16 ? launch(TcTraits<1, 128>{}, fwd_tc_kernel<true, 1, 128>, base + 5)
+              : launch(TcTraits<1, 128>{}, fwd_tc_kernel<false, 1, 128>, base + 4);
+  else if (groups == 2)
     st = bf16 ? launch(TcTraits<2>{}, fwd_tc_kernel<true, 2>, base + 3)
               : launch(TcTraits<2>{}, fwd_tc_kernel<false, 2>, base + 2);
   else

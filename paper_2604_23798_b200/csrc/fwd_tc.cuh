@@ -149,14 +149,19 @@ constexpr bool kTcSelfIssue = ELSA_TC_SELF_ISSUE != 0;
 // anchor hysteresis of the deferred rescale (log2 units): P <= 2^8
 constexpr float kRescaleLog2 = 8.f;
 
-template <int GROUPS>
+// D = 64, or 128 (64 < d, dv <= 128: one query tile per CTA, TMEM holds S,
+// a 128-column W and P; Q/K/V rows as two 64-element swizzle-atom blocks)
+template <int GROUPS, int D_ = 64>
 struct TcTraits {
-  static constexpr int TQ = 128, TK = 128, D = 64, STAGES = ELSA_TC_STAGES;
+  static constexpr int TQ = 128, TK = 128, D = D_;
+  static_assert(D == 64 || (D == 128 && GROUPS == 1), "head width");
+  static constexpr int STAGES = D == 64 ? ELSA_TC_STAGES : 2;  // 2 x 64 KB stages at D = 128
+  static constexpr int DB = D / 64;                          // 128-byte column blocks per row
   static constexpr int ROWS = GROUPS * TQ;                   // query rows per CTA
-  static constexpr int ROW_BYTES = D * 2;                    // 128 B per 16-bit row
-  static constexpr int Q_BYTES = TQ * ROW_BYTES;             // 16 KB per group
-  static constexpr int K_BYTES = TK * ROW_BYTES;             // 16 KB
-  static constexpr int V_BYTES = TK * ROW_BYTES;             // 16 KB
+  static constexpr int Q_BLOCK = TQ * 128, K_BLOCK = TK * 128, V_BLOCK = TK * 128;
+  static constexpr int Q_BYTES = DB * Q_BLOCK;               // 16 KB per group and block
+  static constexpr int K_BYTES = DB * K_BLOCK;
+  static constexpr int V_BYTES = DB * V_BLOCK;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + GROUPS * Q_BYTES;
   static constexpr int OFF_V = OFF_K + STAGES * K_BYTES;
@@ -181,22 +186,22 @@ struct TcTraits {
   static constexpr int THREADS = kRegSplit ? (SOFTMAX_WARPS + 4) * 32 : (SOFTMAX_WARPS + 2) * 32;
   static constexpr int SOFTMAX_REGS = 232, OTHER_REGS = 40;
   static_assert(!kRegSplit || 2 * (SOFTMAX_REGS - 168) <= 168 - OTHER_REGS, "setmaxnreg budget");
-  static constexpr uint32_t TMEM_COLS = GROUPS == 1 ? 256 : 512;
+  static constexpr uint32_t TMEM_COLS = (GROUPS == 1 && D == 64) ? 256 : 512;
   static constexpr uint32_t S_COL = 0;             // group g: S at 128 g
-  static constexpr uint32_t O_COL = 128 * GROUPS;  // group g: W (P V accumulator) at O_COL + 64 g
+  static constexpr uint32_t O_COL = 128 * GROUPS;  // group g: W (P V accumulator) at O_COL + D g
   // group g: P (16-bit, two per 32-bit column) at P_COL + 64 g — the A operand
   // of P V read straight from TMEM (no shared-memory round trip)
-  static constexpr uint32_t P_COL = 192 * GROUPS;
+  static constexpr uint32_t P_COL = (128 + D) * GROUPS;
   static_assert(P_COL + 64 * GROUPS <= TMEM_COLS, "TMEM columns");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
-template <bool kBF16, int GROUPS>
-__global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
+template <bool kBF16, int GROUPS, int D_ = 64>
+__global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
                   const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV) {
-  using T = TcTraits<GROUPS>;
+  using T = TcTraits<GROUPS, D_>;
   extern __shared__ unsigned char smem_dyn[];
   // 1024-byte alignment for the 128B-swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -255,8 +260,9 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     const uint32_t d = tmem + T::S_COL + g * 128;
 #pragma unroll
     for (int kk = 0; kk < T::D / 16; ++kk) {  // K-steps of 16 elements = 32 B
-      const uint64_t a = tc::smem_desc_sw128(q_addr + kk * 32, 16, 1024);
-      const uint64_t bd = tc::smem_desc_sw128(k_addr + kk * 32, 16, 1024);
+      const uint32_t blk = kk >> 2, off = (kk & 3) * 32;  // 64-element column block
+      const uint64_t a = tc::smem_desc_sw128(q_addr + blk * T::Q_BLOCK + off, 16, 1024);
+      const uint64_t bd = tc::smem_desc_sw128(k_addr + blk * T::K_BLOCK + off, 16, 1024);
       if (leader) tc::mma_f16_ss(d, a, bd, kIdescS, kk > 0);
     }
     if (leader) tc::commit(&s_full[g]);
@@ -266,15 +272,19 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
   auto issue_o = [&](int g, int t, int hh, bool leader) {
     const int s = t % T::STAGES;
     const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V + s * T::V_BYTES);
-    const uint32_t d = tmem + T::O_COL + g * 64;
+    const uint32_t d = tmem + T::O_COL + g * T::D;
     const uint32_t pa = tmem + T::P_COL + g * 64;
     constexpr int KS = T::TK / 16 / PH;  // K-steps per part
 #pragma unroll
     for (int k2 = 0; k2 < KS; ++k2) {
       const int kk = hh * KS + k2;
-      // V: MN-major (rows = keys, 128 B each); 16 keys per step = 2 swizzle atoms
-      const uint64_t bd = tc::smem_desc_sw128(v_addr + kk * 2048, 16, 1024);
-      if (leader) tc::mma_f16_ts(d, pa + kk * 8, bd, kIdescO, (t > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+      for (int nb = 0; nb < T::DB; ++nb) {  // 64 output columns per V block
+        // V: MN-major (rows = keys, 128 B each); 16 keys per step = 2 swizzle atoms
+        const uint64_t bd = tc::smem_desc_sw128(v_addr + nb * T::V_BLOCK + kk * 2048, 16, 1024);
+        if (leader)
+          tc::mma_f16_ts(d + nb * 64, pa + kk * 8, bd, kIdescO, (t > 0 || kk > 0) ? 1u : 0u);
+      }
     }
     if (leader) tc::commit(&o_full[g * PH + hh]);
     __syncwarp();
@@ -296,14 +306,20 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       ptx::prefetch_tmap(&tmK);
       ptx::prefetch_tmap(&tmV);
       ptx::mbar_arrive_expect_tx(qbar, GROUPS * T::Q_BYTES);
-      for (int g = 0; g < GROUPS; ++g)  // rows past n_q are zero-filled by TMA
-        ptx::tma_load_4d(smem + T::OFF_Q + g * T::Q_BYTES, &tmQ, qbar, 0, q0 + g * T::TQ, h, b);
+      for (int g = 0; g < GROUPS; ++g)  // rows past n_q / columns past d are zero-filled by TMA
+        for (int blk = 0; blk < T::DB; ++blk)
+          ptx::tma_load_4d(smem + T::OFF_Q + g * T::Q_BYTES + blk * T::Q_BLOCK, &tmQ, qbar,
+                           64 * blk, q0 + g * T::TQ, h, b);
       for (int t = 0; t < ntiles; ++t) {
         const int s = t % T::STAGES;
         if (t >= T::STAGES) ptx::mbar_wait_backoff(&kv_empty[s], ((t / T::STAGES) - 1) & 1, 64);
         ptx::mbar_arrive_expect_tx(&kv_full[s], T::K_BYTES + T::V_BYTES);
-        ptx::tma_load_4d(smem + T::OFF_K + s * T::K_BYTES, &tmK, &kv_full[s], 0, t * T::TK, h, b);
-        ptx::tma_load_4d(smem + T::OFF_V + s * T::V_BYTES, &tmV, &kv_full[s], 0, t * T::TK, h, b);
+        for (int blk = 0; blk < T::DB; ++blk) {
+          ptx::tma_load_4d(smem + T::OFF_K + s * T::K_BYTES + blk * T::K_BLOCK, &tmK, &kv_full[s],
+                           64 * blk, t * T::TK, h, b);
+          ptx::tma_load_4d(smem + T::OFF_V + s * T::V_BYTES + blk * T::V_BLOCK, &tmV, &kv_full[s],
+                           64 * blk, t * T::TK, h, b);
+        }
       }
     }
   } else if (warp == T::MMA_WARP && !kTcSelfIssue) {
@@ -364,7 +380,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
     const int row = (warp & 3) * 32 + lane;
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
     const uint32_t s_tm = tmem + lane_base + T::S_COL + g * 128;
-    const uint32_t o_tm = tmem + lane_base + T::O_COL + g * 64;
+    const uint32_t o_tm = tmem + lane_base + T::O_COL + g * T::D;
     const float c2 = p.c;
     const float cs = p.neg ? -c2 : c2;  // exponent = s_raw * cs - m
     float m_run = -CUDART_INF_F;        // log2-domain anchor
@@ -456,7 +472,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
         tc::fence_after_sync();
         {
 #pragma unroll
-          for (int ch = 0; ch < 2; ++ch) {
+          for (int ch = 0; ch < T::D / 32; ++ch) {
             uint32_t r[32];
             tc::tmem_ld_32x32b_x32(o_tm + ch * 32, r);
             tc::tmem_wait_ld();
@@ -547,13 +563,13 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       if (lane == 0) TC_MARK(warp, t, 5);
     }
     // ---- epilogue: Y = W / S (engine.py:375-382) in the input's 16-bit format ----
-    float w[64];
+    float w[T::D];
     if (ntiles > 0) {
 #pragma unroll
       for (int hh = 0; hh < PH; ++hh) ptx::mbar_wait(&o_full[g * PH + hh], (ntiles - 1) & 1);
       tc::fence_after_sync();
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
+      for (int ch = 0; ch < T::D / 32; ++ch) {
         uint32_t r[32];
         tc::tmem_ld_32x32b_x32(o_tm + ch * 32, r);
         tc::tmem_wait_ld();
@@ -562,7 +578,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 64; ++i) w[i] = 0.f;
+      for (int i = 0; i < T::D; ++i) w[i] = 0.f;
     }
     const int qrow = q0 + g * T::TQ + row;
     if (qrow < p.n_q) {
@@ -571,7 +587,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS>::THREADS, 1)
       unsigned char* yrow = reinterpret_cast<unsigned char*>(p.y) +
                             2 * (int64_t(b) * p.ys_b + int64_t(h) * p.ys_h + int64_t(qrow) * p.ys_r);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < T::D / 8; ++u) {
         if (8 * u >= p.dv) break;
         uint4 pk;
         const float* x = w + 8 * u;

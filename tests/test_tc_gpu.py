@@ -59,14 +59,15 @@ def test_tc_negative_scale_and_determinism():
 
 
 def test_tc_rejects_other_head_dims():
-    q = torch.randn(1, 1, 16, 96, device=DEV, dtype=torch.bfloat16)
+    q = torch.randn(1, 1, 16, 136, device=DEV, dtype=torch.bfloat16)
     with pytest.raises(elsa.ShapeError):
         elsa.scaled_dot_product_attention(q, q, q)
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("d,dv", [(32, 32), (16, 64), (64, 16), (40, 24), (8, 8), (60, 36),
-                                  (3, 5), (64, 1)])
+                                  (3, 5), (64, 1), (128, 128), (96, 80), (128, 64), (64, 128),
+                                  (100, 128), (72, 8)])
 def test_tc_narrow_heads(dtype, d, dv):
     # d, dv < 64: the 64-wide TMA boxes zero-fill past the row (rows not a
     # multiple of 8 elements are first copied into padded rows); Y rows narrower
@@ -123,3 +124,11 @@ def test_tc_random_geometry_fuzz(seed):
     n_q, n_kv = int(rng.integers(1, 900)), int(rng.integers(1, 900))
     scale = None if seed % 3 else float(rng.choice([-1, 1]) * rng.uniform(0.05, 0.2))
     _check(dtype, B, H, n_q, n_kv, seed, scale=scale)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_tc_d128_long_and_ragged(dtype):
+    # the D = 128 kernel (two 64-element column blocks per row, W 128 columns
+    # in TMEM, 2-stage ring) over many key tiles with ragged tails
+    _check(dtype, 2, 3, 1000 + 37, 2048 + 77, seed=5, d=128, dv=128)
+    _check(dtype, 1, 2, 300, 700, seed=6, scale=-0.09, d=128, dv=128)

@@ -32,11 +32,12 @@ def time_fn(fn, iters=20):
     return tot / iters
 
 
+D = int(os.environ.get("D", "64"))  # head width (64, or up to 128: the D = 128 kernel)
 for dt in (torch.bfloat16, torch.float16):
     for (B, H, n) in [(1, 16, 1024), (1, 16, 4096), (1, 16, 16384), (8, 12, 512), (1, 16, 65536)]:
-        q, k, v = (torch.randn(B, H, n, 64, device=dev, dtype=dt) for _ in range(3))
-        flops = 4.0 * B * H * n * n * 64
+        q, k, v = (torch.randn(B, H, n, D, device=dev, dtype=dt) for _ in range(3))
+        flops = 4.0 * B * H * n * n * D
         ms = time_fn(lambda: elsa.scaled_dot_product_attention(q, k, v))
         mt = time_fn(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v))
-        print(f"{str(dt):15s} B{B} H{H} n{n:6d}: elsa {ms:8.3f} ms {flops/ms/1e9:7.1f} TF/s | "
+        print(f"{str(dt):15s} d{D} B{B} H{H} n{n:6d}: elsa {ms:8.3f} ms {flops/ms/1e9:7.1f} TF/s | "
               f"torch {mt:8.3f} ms {flops/mt/1e9:7.1f} TF/s", flush=True)
