@@ -34,7 +34,7 @@ using namespace elsa;
 namespace {
 
 constexpr int kMaxDevices = 64;
-constexpr int kAttrSlots = 28;
+constexpr int kAttrSlots = 32;
 constexpr int kMaxSplits = kMergeMaxParts;
 constexpr double kLog2e = 1.4426950408889634074;
 
@@ -949,7 +949,6 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
   const int64_t BH = shp->B * shp->H;
   int groups = ceil_div(shp->n_q, 256) * BH >= int64_t(dc->sms) ? 2 : 1;
   if (forced_groups == 1 || forced_groups == 2) groups = forced_groups;
-  if (wide16) groups = 1;
   auto launch = [&](auto traits, auto kern, int slot) -> int {
     using TT = decltype(traits);
     p.qtiles = int(ceil_div(shp->n_q, TT::ROWS));
@@ -965,9 +964,12 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
         p, maps[0], maps[1], maps[2]);
     return ELSA_OK;
   };
-  const int base = kAttrSlots - 6;  // the last six slots
+  const int base = kAttrSlots - 8;  // the last eight slots
   int st;
-  if (wide16)
+  if (wide16 && groups == 2)
+    st = bf16 ? launch(TcTraits<2, 128>{}, fwd_tc_kernel<true, 2, 128>, base + 7)
+              : launch(TcTraits<2, 128>{}, fwd_tc_kernel<false, 2, 128>, base + 6);
+  else if (wide16)
     st = bf16 ? launch(TcTraits<1, 128>{}, fwd_tc_kernel<true, 1, 128>, base + 5)
               : launch(TcTraits<1, 128>{}, fwd_tc_kernel<false, 1, 128>, base + 4);
   else if (groups == 2)

@@ -149,12 +149,15 @@ constexpr bool kTcSelfIssue = ELSA_TC_SELF_ISSUE != 0;
 // anchor hysteresis of the deferred rescale (log2 units): P <= 2^8
 constexpr float kRescaleLog2 = 8.f;
 
-// D = 64, or 128 (64 < d, dv <= 128: one query tile per CTA, TMEM holds S,
-// a 128-column W and P; Q/K/V rows as two 64-element swizzle-atom blocks)
+// D = 64, or 128 (64 < d, dv <= 128; Q/K/V rows as two 64-element
+// swizzle-atom blocks). At D = 128, P is written over its own tile's S in
+// TMEM (kAliasP) so that two query tiles (S/P 128 + W 128 columns each) fit
+// the 512 columns; S_g(t+1) is then issued only after P_g(t) V.
 template <int GROUPS, int D_ = 64>
 struct TcTraits {
   static constexpr int TQ = 128, TK = 128, D = D_;
-  static_assert(D == 64 || (D == 128 && GROUPS == 1), "head width");
+  static_assert(D == 64 || D == 128, "head width");
+  static constexpr bool kAliasP = D == 128;
   static constexpr int STAGES = D == 64 ? ELSA_TC_STAGES : 2;  // 2 x 64 KB stages at D = 128
   static constexpr int DB = D / 64;                          // 128-byte column blocks per row
   static constexpr int ROWS = GROUPS * TQ;                   // query rows per CTA
@@ -186,13 +189,17 @@ struct TcTraits {
   static constexpr int THREADS = kRegSplit ? (SOFTMAX_WARPS + 4) * 32 : (SOFTMAX_WARPS + 2) * 32;
   static constexpr int SOFTMAX_REGS = 232, OTHER_REGS = 40;
   static_assert(!kRegSplit || 2 * (SOFTMAX_REGS - 168) <= 168 - OTHER_REGS, "setmaxnreg budget");
-  static constexpr uint32_t TMEM_COLS = (GROUPS == 1 && D == 64) ? 256 : 512;
   static constexpr uint32_t S_COL = 0;             // group g: S at 128 g
   static constexpr uint32_t O_COL = 128 * GROUPS;  // group g: W (P V accumulator) at O_COL + D g
-  // group g: P (16-bit, two per 32-bit column) at P_COL + 64 g — the A operand
-  // of P V read straight from TMEM (no shared-memory round trip)
-  static constexpr uint32_t P_COL = (128 + D) * GROUPS;
-  static_assert(P_COL + 64 * GROUPS <= TMEM_COLS, "TMEM columns");
+  // group g: P (16-bit, two per 32-bit column) at P_COL + P_STRIDE g — the A
+  // operand of P V read straight from TMEM (no shared-memory round trip)
+  static constexpr uint32_t P_COL = kAliasP ? S_COL : (128 + D) * GROUPS;
+  static constexpr uint32_t P_STRIDE = kAliasP ? 128 : 64;
+  static constexpr uint32_t TMEM_NEED = (O_COL + D * GROUPS > P_COL + P_STRIDE * GROUPS)
+                                             ? O_COL + D * GROUPS
+                                             : P_COL + P_STRIDE * GROUPS;
+  static constexpr uint32_t TMEM_COLS = TMEM_NEED <= 256 ? 256 : 512;
+  static_assert(TMEM_NEED <= 512, "TMEM columns");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
@@ -273,7 +280,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
     const int s = t % T::STAGES;
     const uint32_t v_addr = ptx::smem_u32(smem + T::OFF_V + s * T::V_BYTES);
     const uint32_t d = tmem + T::O_COL + g * T::D;
-    const uint32_t pa = tmem + T::P_COL + g * 64;
+    const uint32_t pa = tmem + T::P_COL + g * T::P_STRIDE;
     constexpr int KS = T::TK / 16 / PH;  // K-steps per part
 #pragma unroll
     for (int k2 = 0; k2 < KS; ++k2) {
@@ -364,7 +371,9 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
           }
         }
         const int t = ns[g];
-        if (t < ntiles && (t == 0 || ready(&s_free[g], (t - 1) & 1)) &&
+        // (P aliased over S: S_g(t) only after P_g(t-1) V has been issued)
+        if (t < ntiles && (!T::kAliasP || npv[g] >= t) &&
+            (t == 0 || ready(&s_free[g], (t - 1) & 1)) &&
             ready(&kv_full[t % T::STAGES], (t / T::STAGES) & 1)) {
           tc::fence_after_sync();
           if (lane == 0) TC_MARK(8 + g, t, 0);
@@ -385,7 +394,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
     const float cs = p.neg ? -c2 : c2;  // exponent = s_raw * cs - m
     float m_run = -CUDART_INF_F;        // log2-domain anchor
     float l_run = 0.f;
-    const uint32_t p_tm = tmem + lane_base + T::P_COL + g * 64;
+    const uint32_t p_tm = tmem + lane_base + T::P_COL + g * T::P_STRIDE;
     // self-issue: warp 0 of the group issues the group's MMAs after a
     // group-wide named barrier (id 1 + g) instead of signalling the MMA warp
     const bool issuer = kTcSelfIssue && (warp & 3) == 0;

@@ -132,3 +132,11 @@ def test_tc_d128_long_and_ragged(dtype):
     # in TMEM, 2-stage ring) over many key tiles with ragged tails
     _check(dtype, 2, 3, 1000 + 37, 2048 + 77, seed=5, d=128, dv=128)
     _check(dtype, 1, 2, 300, 700, seed=6, scale=-0.09, d=128, dv=128)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_tc_d128_two_tile_ctas_aliased_p(dtype):
+    # >= one wave of two-query-tile CTAs at d = 128: P written over S in TMEM
+    # and S_g(t+1) issued only after P_g(t) V (ragged rows and key tail)
+    _check(dtype, 1, 16, 2560 + 33, 300 + 5, seed=17, d=128, dv=128)
+    _check(dtype, 2, 8, 2560, 1000, seed=18, scale=-0.1, d=112, dv=96)
