@@ -96,6 +96,11 @@ constexpr bool kTcPackedG2 = ELSA_TC_PACKED_G2 != 0;
 #ifndef ELSA_TC_POLY_EXTRA
 #define ELSA_TC_POLY_EXTRA 0x5555  // bit u: one more polynomial pair in 8-key unit u
 #endif
+#ifndef ELSA_TC_POLY_EXTRA_D128
+// d = 128 (twice the MMA work per exponential) prefers 25%: BF16 16K 0% 1218-1226,
+// 25% 1230, 31% 1220, 37.5% 1198 TFLOP/s
+#define ELSA_TC_POLY_EXTRA_D128 0
+#endif
 #ifndef ELSA_TC_POLY_DEG
 #define ELSA_TC_POLY_DEG 3
 #endif
@@ -514,7 +519,8 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
             x1 = fmaf(s[u * 8 + e + 1], cs, neg_m);
           }
           // this pair on the FMA pipe, the rest on MUFU
-          if (e < 2 * (kTcPolyPairs + ((ELSA_TC_POLY_EXTRA >> u) & 1))) {
+          constexpr unsigned kExtra = T::D == 128 ? ELSA_TC_POLY_EXTRA_D128 : ELSA_TC_POLY_EXTRA;
+          if (e < 2 * (kTcPolyPairs + ((kExtra >> u) & 1))) {
             ex2_poly2(x0, x1, pv[e], pv[e + 1]);
           } else {
             pv[e] = ptx::ex2(x0);
