@@ -474,10 +474,16 @@ def main():
             sweep.append({"comparator": "torch sdpa fp32", "error": str(exc)[:200]})
         # the FP16/BF16 variant (K5, tcgen05) on the same problem, for comparison
         # (BASELINE configs[4]); flops 4*B*H*n^2*64, same as the FP32 count
-        for dt, nm in ((torch.bfloat16, "bf16"), (torch.float16, "fp16")):
+        for dt, nm, dh in ((torch.bfloat16, "bf16", 64), (torch.float16, "fp16", 64),
+                           (torch.bfloat16, "bf16", 128)):
             try:
-                q16, k16, v16 = q.to(dt), k.to(dt), v.to(dt)
-                row = {"variant": f"elsa {nm} (tcgen05)", "B": B, "H": H, "n": n}
+                if dh == 64:
+                    q16, k16, v16 = q.to(dt), k.to(dt), v.to(dt)
+                else:  # wider heads (d = dv = 128), same sequence shape
+                    q16, k16, v16 = (torch.randn(B, H, n, dh, device=dev, generator=gen).to(dt)
+                                     for _ in range(3))
+                fl16 = 4.0 * B * H * n * n * dh
+                row = {"variant": f"elsa {nm} (tcgen05)", "B": B, "H": H, "n": n, "d": dh}
                 for label, fn in (("elsa", lambda: elsa.scaled_dot_product_attention(q16, k16, v16)),
                                   ("torch", lambda: torch.nn.functional.scaled_dot_product_attention(
                                       q16, k16, v16))):
@@ -492,7 +498,7 @@ def main():
                     torch.cuda.synchronize()
                     tms = s0.elapsed_time(s1) / 5
                     row[f"{label}_ms"] = tms
-                    row[f"{label}_tflops"] = fl / (tms * 1e-3) / 1e12
+                    row[f"{label}_tflops"] = fl16 / (tms * 1e-3) / 1e12
                 sweep.append(row)
                 del q16, k16, v16
             except Exception as exc:  # noqa: BLE001
