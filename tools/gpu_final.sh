@@ -10,6 +10,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-sweep --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_$TAG.log 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:fwd_tc -s 1 -c 1 -o gpurun_out/prof_tc16k_$TAG python tools/prof_tc.py > gpurun_out/ncu_tc_$TAG.log 2>&1
 timeout 300 python tools/time_tc.py > gpurun_out/tc_time_$TAG.txt 2>&1
+D=128 timeout 300 python tools/time_tc.py > gpurun_out/tc_time_d128_$TAG.txt 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:fwd_f32 -s 2 -c 1 -o gpurun_out/prof_fwd16k_$TAG python tools/prof_fwd.py --n 16384 --reps 3 > gpurun_out/ncu_full_$TAG.log 2>&1
 ./tools/microbench/ffma_variants > gpurun_out/ffma_variants_$TAG.log 2>&1
 
