@@ -1,36 +1,34 @@
 // fwd_tc.cuh — K5: the FP16 / BF16 variant of the ELSA forward on the 5th-gen
 // tensor cores. The two dense contractions run as
-// tcgen05.mma (kind::f16, FP32 accumulation in TMEM); everything the paper
-// specifies as the ELSA algorithm — the (m, S, W) tile states, their monoid
-// combine, the anchors and the epilogue — stays in FP32 registers exactly as
-// in K1:
-//   S_t = Q K_t^T            tcgen05.mma  128x128x64  -> TMEM (double buffer)
-//   m_t, P_t = 2^(s c - m_t) one query row per thread (tcgen05.ld 32x32b)
-//   O_t = P_t V_t            tcgen05.mma  128x64x128  -> TMEM (double buffer)
-//   W <- (W + O_{t-1}) 2^(m_{t-1} - m_t)   FP32 registers (the ⊕ of monoid.py:160-200)
+// tcgen05.mma (kind::f16, FP32 accumulation in TMEM); the (m, S, W) tile
+// states, their combine, the anchors and the epilogue stay in FP32 as in K1:
+//   S_t = Q K_t^T            tcgen05.mma 128x128xD, A and B from 128B-swizzled smem
+//   P_t = 2^(s c - m)        one query row per thread (tcgen05.ld 32x32b), 16-bit
+//                            P written back to TMEM (tcgen05.st)
+//   W  += P_t V_t            tcgen05.mma 128x64x128 per 64 output columns, A = P
+//                            read from TMEM, W accumulating in TMEM
 //
 // A CTA owns GROUPS (1 or 2) query tiles of 128 rows, one softmax warpgroup
 // each (warp w of group g owns TMEM lanes 32(w%4).. = query rows), so two
-// softmax streams share every SM sub-partition and the single MMA thread
-// ping-pongs between them: while group 0 exponentiates S_0(t), the tensor
-// core computes S_1(t) / P_1 V, and vice versa. Per group TMEM holds S (128
-// columns, single buffer: S(t+1) is issued as soon as the group has loaded
-// S(t) into registers, so it overlaps the group's own exponentials) and the
-// running W = O (64 columns) that P V accumulates into. P goes
-// through a 128B-swizzled smem tile per group (single buffer: written after
-// P(t-1) V completed).
+// softmax streams share every SM sub-partition while the tensor core
+// ping-pongs between them. Per group TMEM holds S (128 columns, single
+// buffer: S_g(t+1) is issued once the group has pulled S_g(t) into registers,
+// overlapping its exponentials), W (D columns) and P (64 packed columns; at
+// D = 128 P is written over the group's own S so two tiles fit 512 columns,
+// and S_g(t+1) then waits for P_g(t) V's issue).
 //
-// The (m, S, W) combine with a deferred anchor: a row's anchor m moves only
-// when the tile maximum exceeds it by more than kRescaleLog2 (log2 units);
-// then S and the TMEM W of that row are multiplied by 2^(m_old - m_new)
-// (tcgen05.ld / st by the owning warp, skipped warp-wide when no row of the
-// warp moved). Between moves every P = 2^(s c - m) <= 2^kRescaleLog2, exact in
-// the 16-bit formats' range; the result is the same monoid product, only the
-// anchor at which each partial sum is represented differs.
+// Combine with a deferred anchor: a row's anchor m moves only when a tile's
+// maximum exceeds it by more than kRescaleLog2 (log2 units); then its running
+// sum and TMEM W row are multiplied by 2^(m_old - m_new) (skipped warp-wide
+// when no row of the warp moved). Between moves every P <= 2^kRescaleLog2,
+// exact in the 16-bit formats' range: the same monoid product, represented
+// at a different anchor. A share of the exponentials runs as an FFMA2
+// polynomial (MUFU.EX2 is the softmax's binding pipe).
 //
-// Warp roles (GROUPS*128 + 64 threads, 1 CTA / SM): softmax warpgroups, then
-// a TMA producer warp (Q once, K/V through a 3-stage ring, 128B-swizzled
-// 16-bit tiles) and the TMEM allocator + single-thread MMA issuer warp.
+// Warp roles: softmax warpgroups, then a TMA producer warp (Q once, K/V
+// through a STAGES-deep ring) and the TMEM allocator + MMA warp (a
+// warp-uniform event loop, one elected lane issues). GROUPS = 2 adds two idle
+// warps so setmaxnreg can hand a whole warpgroup's registers to the softmax.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
