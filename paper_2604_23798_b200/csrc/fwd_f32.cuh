@@ -34,9 +34,12 @@
 //   rows   r_i = 2R*warp + rg + 2i,  i = 0..R-1   (both GEMMs)
 //   GEMM1  keys g + 16j,  j = 0..RK-1             (S micro-tile R x RK)
 //   GEMM2  cols 4g .. 4g+3                        (O micro-tile R x 4)
-// Shared layouts: raw Q/K rows TMA-boxed 68 floats wide (4 zero columns pad
-// the pitch to 272 B); Q^T[d][row position] with each lane's R rows
-// contiguous; P^T[key][row position] per warp, pitch 2R+4.
+// Shared layouts: raw Q/K rows TMA-boxed D + 4 floats wide (D = 32 / 64 /
+// 96 / 128 / 256; the 4 zero columns pad the pitch off the bank period);
+// Q^T[d][row position] with each lane's R rows contiguous; P^T[key][row
+// position] per warp, pitch 2R+4. V in DV-column slices (32 / 64 / 128;
+// wider V runs on grid z). Operands TMA cannot describe go through a cp.async
+// copy engine into the same layouts.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
