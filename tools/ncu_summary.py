@@ -42,7 +42,11 @@ def main():
     ap.add_argument("--h", type=int, default=16)
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--d", type=int, default=64)
-    ap.add_argument("--peak", type=float, default=74.45, help="FFMA peak TFLOP/s")
+    ap.add_argument("--dv", type=int, default=None, help="V width (default: d)")
+    ap.add_argument("--elem-bytes", type=int, default=4, help="4 (FP32) or 2 (FP16/BF16)")
+    ap.add_argument("--peak", type=float, default=74.45,
+                    help="TFLOP/s denominator: FFMA peak (74.45) for K1, the measured dense "
+                         "BF16 peak (MEASURED_PEAKS.json bf16_tflops) for K5")
     a = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
@@ -74,9 +78,10 @@ def main():
                 stalls[k.replace("smsp__average_warps_issue_stalled_", "").replace(
                     "_per_issue_active.ratio", "")] = round(x, 3)
     out["stalls_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1]))
-    flops = 2.0 * a.b * a.h * a.n * a.n * (a.d + a.d)
-    alg_bytes = 4.0 * a.b * a.h * a.n * a.d * 4
-    out["workload"] = f"B{a.b} H{a.h} n{a.n} d{a.d}"
+    dv = a.d if a.dv is None else a.dv
+    flops = 2.0 * a.b * a.h * a.n * a.n * (a.d + dv)
+    alg_bytes = float(a.elem_bytes) * a.b * a.h * a.n * (2 * a.d + 2 * dv)
+    out["workload"] = f"B{a.b} H{a.h} n{a.n} d{a.d} dv{dv} ({a.elem_bytes}-byte elements)"
     out["algorithmic_flops"] = flops
     out["algorithmic_bytes"] = alg_bytes
     if out.get("dram_read_bytes") is not None:
@@ -84,7 +89,8 @@ def main():
         out["traffic_over_algorithmic"] = out["dram_bytes_per_launch"] / alg_bytes
     if out.get("duration_ms"):
         out["tflops_under_ncu"] = flops / (out["duration_ms"] * 1e-3) / 1e12
-        out["frac_ffma_peak_under_ncu"] = out["tflops_under_ncu"] / a.peak
+        out["peak_tflops"] = a.peak
+        out["frac_peak_under_ncu"] = out["tflops_under_ncu"] / a.peak
     os.makedirs("profiles", exist_ok=True)
     with open(f"profiles/{a.tag}.json", "w") as f:
         json.dump(out, f, indent=2)

@@ -14,9 +14,12 @@ ap.add_argument("--h", type=int, default=16)
 ap.add_argument("--n", type=int, default=16384)
 ap.add_argument("--reps", type=int, default=4)
 ap.add_argument("--splits", type=int, default=0)
+ap.add_argument("--d", type=int, default=64)
+ap.add_argument("--dv", type=int, default=64)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
-q, k, v = (torch.randn(a.b, a.h, a.n, 64, device=dev) for _ in range(3))
+q, k = (torch.randn(a.b, a.h, a.n, a.d, device=dev) for _ in range(2))
+v = torch.randn(a.b, a.h, a.n, a.dv, device=dev)
 for _ in range(a.reps):
     elsa.scaled_dot_product_attention(q, k, v, kv_splits=a.splits)
 torch.cuda.synchronize()
