@@ -165,10 +165,16 @@ struct FwdTraits {
   static constexpr int WR = 2 * R;        // query rows per warp
   static constexpr int D = D_;            // padded head width of Q/K: 64, 96, 128 or 256
   static constexpr int DV = DV_;          // V columns per CTA (32, 64 or 128); wider V runs as slices (grid z)
-  static constexpr int CV = DV / 16;      // GEMM2 columns per lane: VW g + 16 VW v + c, v < NVL, c < VW
-  static constexpr int VW = DV >= 64 ? 4 : DV / 16;  // V floats per lane per load
-  static constexpr int NVL = DV / (16 * VW);          // V loads per key per lane
-  static constexpr int NV4 = VW == 4 ? NVL : 0;       // (float4 loads: the DV >= 64 kernels)
+  static constexpr int CV = DV / 16;      // GEMM2 columns per lane
+  static constexpr int VW = DV >= 64 ? 4 : DV / 16;  // V floats per lane per load (segment 0)
+  static constexpr int NVL = DV == 96 ? 2 : DV / (16 * VW);  // V loads per key per lane
+  // A lane's GEMM2 columns come in segments: segment q covers columns
+  // SEG_BASE(q) + SEG_W(q) g + c, c < SEG_W(q), accumulators SEG_C0(q) + c.
+  // DV = 32: (0, 2); 64: (0, 4); 96: (0, 4) (64, 2); 128: (0, 4) (64, 4).
+  static constexpr int NSEG = DV == 96 ? 2 : NVL;
+  __host__ __device__ static constexpr int SEG_W(int q) { return DV == 96 ? (q == 0 ? 4 : 2) : VW; }
+  __host__ __device__ static constexpr int SEG_BASE(int q) { return DV == 96 ? 64 * q : 16 * VW * q; }
+  __host__ __device__ static constexpr int SEG_C0(int q) { return DV == 96 ? 4 * q : VW * q; }
   static constexpr int TQ = WR * W;
   static constexpr int QP = D + 4;        // raw Q / K row pitch in floats (272 B; TMA box width)
   static constexpr int QTP = TQ;          // Q^T pitch: Qt[d][row position]
@@ -238,7 +244,7 @@ struct FwdTraits {
   static constexpr uint32_t Q_TX_BYTES = uint32_t(QRAW_FLOATS) * 4;
   static_assert(TK % 16 == 0, "TK must be a multiple of 16");
   static_assert(R % 4 == 0, "R must be a multiple of 4 (float4 row groups)");
-  static_assert(DV == 32 || DV == 64 || DV == 128, "V slice width");
+  static_assert(DV == 32 || DV == 64 || DV == 96 || DV == 128, "V slice width");
   static_assert(RK % PH == 0, "P halves split the lane's GEMM1 keys evenly");
   static_assert(TQ <= 256, "TMA box rows <= 256");
   static_assert(!kQtDirect || QP > 256, "direct Q^T copies only in copy-engine-only kernels");
@@ -482,7 +488,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   // P area (rows jj - k0)
   auto gemm2 = [&](int tt, int k0) {
     const int st = tt % T::STAGES;
-    const float* vs = Vs + st * T::V_FLOATS + T::VW * g;
+    const float* vs = Vs + st * T::V_FLOATS;
 #pragma unroll(T::G2_UNROLL)
     for (int jj = 0; jj < TK / T::PH; ++jj) {
       f32x2 pr[RP];
@@ -491,14 +497,15 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
         ptx::lds128x2(ptr + jj * PTP + 4 * u, pr[2 * u], pr[2 * u + 1]);
       float va[CV];
 #pragma unroll
-      for (int q = 0; q < T::NVL; ++q) {
-        const float* src = vs + (k0 + jj) * VP + 16 * T::VW * q;
-        if constexpr (T::VW == 4) {
+      for (int q = 0; q < T::NSEG; ++q) {
+        const float* src = vs + (k0 + jj) * VP + T::SEG_BASE(q) + T::SEG_W(q) * g;
+        float* dst = va + T::SEG_C0(q);
+        if (T::SEG_W(q) == 4) {
           const float4 f = ptx::lds128(src);
-          va[4 * q] = f.x, va[4 * q + 1] = f.y, va[4 * q + 2] = f.z, va[4 * q + 3] = f.w;
+          dst[0] = f.x, dst[1] = f.y, dst[2] = f.z, dst[3] = f.w;
         } else {
           const float2 f = *reinterpret_cast<const float2*>(src);
-          va[2 * q] = f.x, va[2 * q + 1] = f.y;
+          dst[0] = f.x, dst[1] = f.y;
         }
       }
 #pragma unroll
@@ -516,7 +523,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   // ... then release the tile's K/V stage to the producer.
   auto gemm2_release = [&](int tt) {
     const int st = tt % T::STAGES;
-    if constexpr (T::NV4 == 1 && T::PH == 1) {
+    if constexpr (T::DV == 64 && T::PH == 1) {
       // the d <= 64 / dv <= 64 kernels: this exact form (ptxas schedules the
       // generalised loop differently)
       const float* vs = Vs + st * T::V_FLOATS + 4 * g;
@@ -706,19 +713,34 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
 #pragma unroll
         for (int c = 0; c < CV; ++c) yv[c] = __fdiv_rn(o[c], l);
 #pragma unroll
-        for (int v4 = 0; v4 < T::NVL; ++v4) {
-          constexpr int VW = T::VW;
-          const int col = col0 + 16 * VW * v4 + VW * g;
-          const float* yq = yv + VW * v4;
-          if (p.y_vec && col + VW - 1 < p.dv) {
-            if constexpr (VW == 4)
-              *reinterpret_cast<float4*>(yrow + col) = make_float4(yq[0], yq[1], yq[2], yq[3]);
-            else
-              *reinterpret_cast<float2*>(yrow + col) = make_float2(yq[0], yq[1]);
-          } else {
+        for (int v4 = 0; v4 < T::NSEG; ++v4) {
+          if constexpr (T::DV != 96) {  // uniform segments (compile-time width)
+            constexpr int VW = T::VW;
+            const int col = col0 + 16 * VW * v4 + VW * g;
+            const float* yq = yv + VW * v4;
+            if (p.y_vec && col + VW - 1 < p.dv) {
+              if constexpr (VW == 4)
+                *reinterpret_cast<float4*>(yrow + col) = make_float4(yq[0], yq[1], yq[2], yq[3]);
+              else
+                *reinterpret_cast<float2*>(yrow + col) = make_float2(yq[0], yq[1]);
+            } else {
 #pragma unroll
-            for (int c = 0; c < VW; ++c)
-              if (col + c < p.dv) yrow[col + c] = yq[c];
+              for (int c = 0; c < VW; ++c)
+                if (col + c < p.dv) yrow[col + c] = yq[c];
+            }
+          } else {  // DV = 96: a 4-wide and a 2-wide segment
+            const int VW = T::SEG_W(v4);
+            const int col = col0 + T::SEG_BASE(v4) + VW * g;
+            const float* yq = yv + T::SEG_C0(v4);
+            if (p.y_vec && col + VW - 1 < p.dv) {
+              if (VW == 4)
+                *reinterpret_cast<float4*>(yrow + col) = make_float4(yq[0], yq[1], yq[2], yq[3]);
+              else
+                *reinterpret_cast<float2*>(yrow + col) = make_float2(yq[0], yq[1]);
+            } else {
+              for (int c = 0; c < VW; ++c)
+                if (col + c < p.dv) yrow[col + c] = yq[c];
+            }
           }
         }
       } else {
@@ -731,19 +753,34 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
         }
         float* wrow = p.pW + idx * p.pw_pitch;
 #pragma unroll
-        for (int v4 = 0; v4 < T::NVL; ++v4) {
-          constexpr int VW = T::VW;
-          const int col = col0 + 16 * VW * v4 + VW * g;
-          const float* oq = o + VW * v4;
-          if (p.pw_vec && col + VW - 1 < p.dv) {
-            if constexpr (VW == 4)
-              *reinterpret_cast<float4*>(wrow + col) = make_float4(oq[0], oq[1], oq[2], oq[3]);
-            else
-              *reinterpret_cast<float2*>(wrow + col) = make_float2(oq[0], oq[1]);
-          } else {
+        for (int v4 = 0; v4 < T::NSEG; ++v4) {
+          if constexpr (T::DV != 96) {  // uniform segments (compile-time width)
+            constexpr int VW = T::VW;
+            const int col = col0 + 16 * VW * v4 + VW * g;
+            const float* oq = o + VW * v4;
+            if (p.pw_vec && col + VW - 1 < p.dv) {
+              if constexpr (VW == 4)
+                *reinterpret_cast<float4*>(wrow + col) = make_float4(oq[0], oq[1], oq[2], oq[3]);
+              else
+                *reinterpret_cast<float2*>(wrow + col) = make_float2(oq[0], oq[1]);
+            } else {
 #pragma unroll
-            for (int c = 0; c < VW; ++c)
-              if (col + c < p.dv) wrow[col + c] = oq[c];
+              for (int c = 0; c < VW; ++c)
+                if (col + c < p.dv) wrow[col + c] = oq[c];
+            }
+          } else {  // DV = 96: a 4-wide and a 2-wide segment
+            const int VW = T::SEG_W(v4);
+            const int col = col0 + T::SEG_BASE(v4) + VW * g;
+            const float* oq = o + T::SEG_C0(v4);
+            if (p.pw_vec && col + VW - 1 < p.dv) {
+              if (VW == 4)
+                *reinterpret_cast<float4*>(wrow + col) = make_float4(oq[0], oq[1], oq[2], oq[3]);
+              else
+                *reinterpret_cast<float2*>(wrow + col) = make_float2(oq[0], oq[1]);
+            } else {
+              for (int c = 0; c < VW; ++c)
+                if (col + c < p.dv) wrow[col + c] = oq[c];
+            }
           }
         }
       }
