@@ -34,7 +34,7 @@ using namespace elsa;
 namespace {
 
 constexpr int kMaxDevices = 64;
-constexpr int kAttrSlots = 36;
+constexpr int kAttrSlots = 38;
 constexpr int kMaxSplits = kMergeMaxParts;
 constexpr double kLog2e = 1.4426950408889634074;
 
@@ -138,10 +138,12 @@ enum CfgId {
   kCfgW8R8D96V96 = 11,  // 64 < d, dv <= 96: 96 V columns (6 per lane)
   kCfgW8R8V96 = 12,     // d <= 64 < dv <= 96
   kCfgW8R8D128V96 = 13, // 96 < d <= 128, 64 < dv <= 96
+  kCfgW4R8D256V256 = 14,  // 128 < d <= 256, dv > 128: 256 V columns per CTA (one S per tile)
   kCfgAuto = -1
 };
 int cfg_dv(int cfg) {
   if (cfg == kCfgW8R8D32V32) return 32;
+  if (cfg == kCfgW4R8D256V256) return 256;
   if (cfg == kCfgW8R8D96V96 || cfg == kCfgW8R8V96 || cfg == kCfgW8R8D128V96) return 96;
   return (cfg == kCfgW8R8V128 || cfg == kCfgW8R8D128V128 || cfg == kCfgW8R8D96V128 ||
           cfg == kCfgW4R8D256V128)
@@ -156,7 +158,8 @@ int wide_cfg(int64_t d, int64_t dv) {
   if (d <= 96) return v ? (dv <= 96 ? int(kCfgW8R8D96V96) : int(kCfgW8R8D96V128)) : int(kCfgW8R8D96);
   if (d <= 128)
     return v ? (dv <= 96 ? int(kCfgW8R8D128V96) : int(kCfgW8R8D128V128)) : int(kCfgW8R8D128);
-  return v ? int(kCfgW4R8D256V128) : int(kCfgW8R8D256);
+  if (!v) return int(kCfgW8R8D256);
+  return dv <= 128 ? int(kCfgW4R8D256V128) : int(kCfgW4R8D256V256);
 }
 constexpr int64_t kMaxD = 256;
 constexpr int64_t kMaxDv = 4096;
@@ -213,6 +216,8 @@ CfgInfo cfg_info(int cfg) {
       return {128, 64, 1, 6.7, 5.2};
     case kCfgW8R8D128V96:
       return {128, 64, 1, 9.4, 7.2};
+    case kCfgW4R8D256V256:
+      return {64, 32, 1, 7.0, 5.0};
     default:
       return {64, 64, 2, 2.711, 1.6};
   }
@@ -452,6 +457,9 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
     case kCfgW8R8D128V96:
       return launch_fwd_cfg<8, 64, 2, 8, 128, 96>(p, s, q_st, k_st, v_st, splits, bh_count,
                                                   kCfgW8R8D128V96, dc, stream);
+    case kCfgW4R8D256V256:
+      return launch_fwd_cfg<4, 32, 2, 8, 256, 256>(p, s, q_st, k_st, v_st, splits, bh_count,
+                                                   kCfgW4R8D256V256, dc, stream);
     default:
       return launch_fwd_cfg<4, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW4R8, dc,
                                          stream);
@@ -1280,9 +1288,9 @@ int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n
   static const char* names[] = {"w4r8",     "w8r16",        "w8r8",    "w8r8d128",
                                 "w8r8v128", "w8r8d128v128", "w8r8d96", "w8r8d96v128",
                                 "w8r8d256", "w4r8d256v128", "w8r8d32v32", "w8r8d96v96",
-                                "w8r8v96", "w8r8d128v96"};
-  static_assert(sizeof(names) / sizeof(names[0]) == kCfgW8R8D128V96 + 1, "one name per config");
-  if (pl.cfg < 0 || pl.cfg > kCfgW8R8D128V96) return ELSA_ERR_SHAPE;
+                                "w8r8v96", "w8r8d128v96", "w4r8d256v256"};
+  static_assert(sizeof(names) / sizeof(names[0]) == kCfgW4R8D256V256 + 1, "one name per config");
+  if (pl.cfg < 0 || pl.cfg > kCfgW4R8D256V256) return ELSA_ERR_SHAPE;
   const CfgInfo ci = cfg_info(pl.cfg);
   const int64_t slices = ceil_div(shp->dv, cfg_dv(pl.cfg));
   std::snprintf(buf, n, "%s tq=%d tk=%d kv_splits=%d heads_per_batch=%lld%s", names[pl.cfg],

@@ -170,7 +170,8 @@ struct FwdTraits {
   static constexpr int NVL = DV == 96 ? 2 : DV / (16 * VW);  // V loads per key per lane
   // A lane's GEMM2 columns come in segments: segment q covers columns
   // SEG_BASE(q) + SEG_W(q) g + c, c < SEG_W(q), accumulators SEG_C0(q) + c.
-  // DV = 32: (0, 2); 64: (0, 4); 96: (0, 4) (64, 2); 128: (0, 4) (64, 4).
+  // DV = 32: (0, 2); 64: (0, 4); 96: (0, 4) (64, 2); 128: (0, 4) (64, 4);
+  // 256: four 4-wide segments at 0, 64, 128, 192.
   static constexpr int NSEG = DV == 96 ? 2 : NVL;
   __host__ __device__ static constexpr int SEG_W(int q) { return DV == 96 ? (q == 0 ? 4 : 2) : VW; }
   __host__ __device__ static constexpr int SEG_BASE(int q) { return DV == 96 ? 64 * q : 16 * VW * q; }
@@ -244,7 +245,7 @@ struct FwdTraits {
   static constexpr uint32_t Q_TX_BYTES = uint32_t(QRAW_FLOATS) * 4;
   static_assert(TK % 16 == 0, "TK must be a multiple of 16");
   static_assert(R % 4 == 0, "R must be a multiple of 4 (float4 row groups)");
-  static_assert(DV == 32 || DV == 64 || DV == 96 || DV == 128, "V slice width");
+  static_assert(DV == 32 || DV == 64 || DV == 96 || DV == 128 || DV == 256, "V slice width");
   static_assert(RK % PH == 0, "P halves split the lane's GEMM1 keys evenly");
   static_assert(TQ <= 256, "TMA box rows <= 256");
   static_assert(!kQtDirect || QP > 256, "direct Q^T copies only in copy-engine-only kernels");

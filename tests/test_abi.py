@@ -170,6 +170,7 @@ def test_describe_plan_names_every_width_configuration():
     want = {(64, 64): ("w8r8", "w4r8", "w8r16"), (128, 64): ("w8r8d128",), (64, 128): ("w8r8v128",),
             (128, 128): ("w8r8d128v128",), (96, 96): ("w8r8d96v96",), (80, 40): ("w8r8d96",),
             (90, 100): ("w8r8d96v128",), (64, 96): ("w8r8v96",), (128, 80): ("w8r8d128v96",),
+            (256, 256): ("w4r8d256v256",),
             (256, 64): ("w8r8d256",), (200, 100): ("w4r8d256v128",), (32, 32): ("w8r8d32v32",),
             (32, 40): ("w8r8", "w4r8", "w8r16")}
     for (d, dv), names in want.items():

@@ -46,7 +46,7 @@ def _bound(y, ref, n, what):
     (128, 128), (128, 64), (64, 128), (96, 96), (80, 200), (65, 65), (127, 1), (100, 130),
     (128, 256), (16, 192), (128, 8), (96, 64), (88, 40), (72, 128), (256, 256), (192, 64),
     (200, 130), (129, 1), (256, 40), (32, 32), (17, 29), (32, 8), (4, 32), (96, 90), (70, 80),
-    (96, 65), (64, 96), (128, 90), (100, 70)])
+    (96, 65), (64, 96), (128, 90), (100, 70), (200, 200), (192, 256), (256, 300)])
 @pytest.mark.parametrize("splits", [1, 3])
 def test_wide_heads_vs_fp64(d, dv, splits):
     n = 333
