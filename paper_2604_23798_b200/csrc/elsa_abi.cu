@@ -975,7 +975,12 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
     return e ? std::atoi(e) : 0;
   }();
   const int64_t BH = shp->B * shp->H;
-  int groups = ceil_div(shp->n_q, 256) * BH >= int64_t(dc->sms) ? 2 : 1;
+  // waves of one-tile vs two-tile CTAs; a two-tile CTA takes ~1.4x a one-tile
+  // CTA's time (measured: B1 H16 n = 1K one-tile 16.4 vs 20.4 us, n = 2K
+  // two-tile 34.8 vs 43.0 us, BERT-base two-tile 26.6 vs 28.7 us)
+  const int64_t waves1 = ceil_div(ceil_div(shp->n_q, 128) * BH, dc->sms);
+  const int64_t waves2 = ceil_div(ceil_div(shp->n_q, 256) * BH, dc->sms);
+  int groups = 1.4 * double(waves2) <= double(waves1) ? 2 : 1;
   if (forced_groups == 1 || forced_groups == 2) groups = forced_groups;
   auto launch = [&](auto traits, auto kern, int slot) -> int {
     using TT = decltype(traits);
