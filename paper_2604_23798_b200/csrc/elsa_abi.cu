@@ -34,6 +34,12 @@ using namespace elsa;
 namespace {
 
 constexpr int kMaxDevices = 64;
+#ifndef ELSA_W8R8_STAGES
+#define ELSA_W8R8_STAGES 3  // K/V ring depth of w8r8 (3: +0.5% at 8K-16K, tools/ab_time.py; w4r8 at 3 stages loses its second CTA per SM: 4K 54.6 -> 49.5)
+#endif
+#ifndef ELSA_W4R8_STAGES
+#define ELSA_W4R8_STAGES 2
+#endif
 constexpr int kAttrSlots = 38;
 constexpr int kMaxSplits = kMergeMaxParts;
 constexpr double kLog2e = 1.4426950408889634074;
@@ -422,7 +428,7 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
       return launch_fwd_cfg<8, 64, 2, 16>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R16, dc,
                                           stream);
     case kCfgW8R8:
-      return launch_fwd_cfg<8, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8, dc,
+      return launch_fwd_cfg<8, 64, ELSA_W8R8_STAGES, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8, dc,
                                          stream);
     case kCfgW8R8D128:
       return launch_fwd_cfg<8, 64, 2, 8, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
@@ -461,7 +467,7 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
       return launch_fwd_cfg<4, 32, 2, 8, 256, 256>(p, s, q_st, k_st, v_st, splits, bh_count,
                                                    kCfgW4R8D256V256, dc, stream);
     default:
-      return launch_fwd_cfg<4, 64, 2, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW4R8, dc,
+      return launch_fwd_cfg<4, 64, ELSA_W4R8_STAGES, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW4R8, dc,
                                          stream);
   }
 }
