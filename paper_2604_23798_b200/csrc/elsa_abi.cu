@@ -37,6 +37,9 @@ constexpr int kMaxDevices = 64;
 #ifndef ELSA_W8R8_STAGES
 #define ELSA_W8R8_STAGES 3  // K/V ring depth of w8r8 (3: +0.5% at 8K-16K, tools/ab_time.py; w4r8 at 3 stages loses its second CTA per SM: 4K 54.6 -> 49.5)
 #endif
+#ifndef ELSA_D32_STAGES
+#define ELSA_D32_STAGES 4  // K/V ring depth of w8r8d32v32 (2: 11.50, 3: 11.47, 4: 11.45 ms at B1 H16 n16K)
+#endif
 #ifndef ELSA_W4R8_STAGES
 #define ELSA_W4R8_STAGES 2
 #endif
@@ -452,7 +455,7 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
       return launch_fwd_cfg<4, 32, 2, 8, 256, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
                                                    kCfgW4R8D256V128, dc, stream);
     case kCfgW8R8D32V32:
-      return launch_fwd_cfg<8, 64, 2, 8, 32, 32>(p, s, q_st, k_st, v_st, splits, bh_count,
+      return launch_fwd_cfg<8, 64, ELSA_D32_STAGES, 8, 32, 32>(p, s, q_st, k_st, v_st, splits, bh_count,
                                                  kCfgW8R8D32V32, dc, stream);
     case kCfgW8R8D96V96:
       return launch_fwd_cfg<8, 64, 2, 8, 96, 96>(p, s, q_st, k_st, v_st, splits, bh_count,
