@@ -177,6 +177,24 @@ def cpu_baseline_sample(n, heads, batch, tiles, workers):
     return fl / dt / 1e12, dt, desc
 
 
+def cpu_full_configs(workers):
+    """the reference CPU algorithm timed in full on the small
+    BASELINE configs (C1, C2 and C3 at n = 1K), on the same host threads."""
+    import oracle
+
+    rows = []
+    for name, (B, H, n) in (("C1", (1, 1, 1024)), ("C2 BERT-base", (8, 12, 512)),
+                            ("C3 n=1K", (1, 16, 1024))):
+        Q, K, V = oracle.generate(0, "regular", b=B, h=H, n=n, d=64, d_v=64, dtype=np.float32)
+        t0 = time.perf_counter()
+        oracle.scan_forward_port(Q, K, V, block_size=128, tile_q=64, workers=workers)
+        dt = time.perf_counter() - t0
+        rows.append({"config": name, "B": B, "H": H, "n": n, "seconds": dt,
+                     "tflops": flops(B, H, n, n) / dt / 1e12, "cores": workers,
+                     "kind": "port", "timed": "full problem"})
+    return rows
+
+
 def _cpu_workers(args):
     cores = os.cpu_count() or 1
     # each worker holds ~0.8 GB of (T, n, d_v) scan lanes at n = 16K; bound RAM
@@ -511,7 +529,8 @@ def main():
         tiles = args.cpu_sample_tiles or workers
         val, secs, desc = cpu_baseline_sample(n, H, B, tiles, workers)
         cpu = {"value": val, "unit": "TFLOP/s", "cores": workers, "kind": "port",
-               "sample": desc, "seconds": secs}
+               "sample": desc, "seconds": secs,
+               "full_small_configs": cpu_full_configs(workers)}
 
     if sharded and args.shard == "kv":
         # per-rank working set of one step: all of Q, this rank's K/V shard and
