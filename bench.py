@@ -3,21 +3,32 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl elsa|reference]
 
-Workload (BASELINE.json configs[2], the config its metric is quoted on):
-FP32 attention B=1 H=16 d=dv=64 at n=16384 — one "step" is one full forward
-over the (B, H, n, d) problem. The headline `value` is whole-job TFLOP/s with
+Headline workload (BASELINE.json configs[2], the config its metric is quoted
+on): FP32 attention B=1 H=16 d=dv=64 at n=16384 per GPU — one "step" is one
+full forward over the (B, H, n, d) problem. `value` is whole-job TFLOP/s with
 algorithmic flops 2*B*H*n^2*(d+dv) (QK^T + PV, FMA = 2; exps not counted),
 inputs resident in HBM (3 x 67 MB > the 126 MB L2, so consecutive steps do not
-hit in L2). `e2e` is the same metric through the public drop-in
-(`paper_2604_23798_b200.attention_from_host` -> C-ABI `elsa_fwd_f32_host`)
-with pinned host buffers: H2D of Q/K/V and D2H of Y inside the timed region,
-pipelined per head group under the kernels. The 1K..16K sweep
-(plus BERT-base and the single-head config) is reported beside it with the
-L2 flushed between timed iterations.
+hit in L2). `e2e` is the same metric through the public host-buffer entry
+point (`paper_2604_23798_b200.attention_from_host` -> C-ABI
+`elsa_fwd_f32_host`) with pinned host buffers: H2D of Q/K/V and D2H of Y
+inside the timed region, pipelined per head group under the kernels.
+`parity` checks sampled rows of the Y the timed steps produced against FP64.
 
-N > 1 (torchrun, one rank per GPU, NCCL): the same problem KV-sharded across
-the ranks (paper_2604_23798_b200.dist: per-chunk (m,S,W) states, one
-all_to_all, fixed (+)-tree merge) — strong scaling of a fixed problem.
+N > 1 (torchrun, one rank per GPU, NCCL): the work shards over batch x heads
+(BASELINE north_star) — the global problem is B=N (one C3-16K problem per
+GPU), split into contiguous (b, h, q) row slices by
+`dist.query_sharded_attention`, no data-path collective (`scaling: weak`).
+`strong` times the fixed B=1 problem over the same row slicing.
+
+`long_context` (every N): C4 (B1 H16 n=65536) and C5 (B1 H8 n=2^20) — at
+N = 1 the single-GPU forward, at N > 1 KV-sharded over the ranks
+(Proposition 1: per-chunk (m, S, W) states, fused
+peer-memory merge over NVLink), strong scaling of a fixed problem, each with
+FP64 sampled-row parity.
+
+The sweep (N = 1: 1K..16K, BERT-base, the single-head config, the FP32 SDPA
+comparator and the 16-bit tcgen05 variant) flushes the L2 between timed
+iterations.
 
 `--impl reference` times the reference's own CPU algorithm (the blocked
 scan of scanattn.engine.scan_forward, restated bit-exactly in
@@ -28,6 +39,7 @@ workload (whole 64-query tiles), and reports the same metric.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import math
 import os
@@ -45,10 +57,22 @@ METRIC = ("FP32 attention ms & TFLOP/s vs seq len 1K–16K; % of FP32 FFMA peak;
           "1/2/4/8 GPU")
 SMS = 148
 FFMA_LANES = 128
+U32 = 2.0 ** -24
 
 
 def flops(b, h, n_q, n_kv, d=64, dv=64):
     return 2.0 * b * h * n_q * n_kv * (d + dv)
+
+
+def scan_depth(n, block=128):
+    """L(n, B) of engine.py:47-55 (the parity bound's depth factor)."""
+    def clog2(x):
+        return 0 if x <= 1 else (int(x) - 1).bit_length()
+    return clog2(min(block, n)) + 2 * clog2(-(-n // block)) + 3
+
+
+def bound(n):
+    return U32 * scan_depth(n) * 8
 
 
 def parse():
@@ -59,22 +83,25 @@ def parse():
     ap.add_argument("--impl", choices=["elsa", "reference"], default="elsa")
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--heads", type=int, default=16)
-    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--batch", type=int, default=1, help="batch per GPU")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--long", default="c4,c5",
+                    help="long-context configs to time at every N (comma list of c4, c5; "
+                         "'none' to skip)")
     ap.add_argument("--cpu-sample-tiles", type=int, default=0,
                     help="64-query tiles per CPU sample (0 = one per worker)")
     ap.add_argument("--cpu-workers", type=int, default=0)
     ap.add_argument("--dist-path", action="store_true",
-                    help="run the KV-sharded multi-GPU code path even at N = 1 (a world-size-1 "
-                         "NCCL group; checks the N > 1 path on a single GPU)")
-    ap.add_argument("--shard", choices=["kv", "q"], default="kv",
-                    help="N > 1: KV-sharded (Proposition 1, the product) or query-sharded "
-                         "(no exchange; SURVEY 8e's control experiment)")
-    ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
-                    help="N > 1: state exchange + merge over symmetric peer memory (one "
-                         "kernel) or NCCL all_to_all + merge kernel")
+                    help="run the N > 1 code paths even at N = 1 (a world-size-1 NCCL group)")
+    ap.add_argument("--shard", choices=["q", "kv"], default="q",
+                    help="headline at N > 1: batch x heads row slices (no exchange, the "
+                         "natural sharding) or KV-sharded (Proposition 1)")
+    ap.add_argument("--exchange", choices=["auto", "peer", "nccl"], default="auto",
+                    help="KV-sharded runs: fused symmetric-memory peer merge or NCCL "
+                         "all_to_all + merge kernel (auto = peer on NCCL groups)")
     return ap.parse_args()
 
 
@@ -157,6 +184,49 @@ def ncu_traffic():
         return None, None
 
 
+def host_info():
+    """The host the CPU baseline runs on (engine.py:88-89: the reference's
+    default is workers='auto' -> os.cpu_count())."""
+    cores = os.cpu_count() or 1
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = cores
+    try:
+        import psutil
+        mem_gb = psutil.virtual_memory().available / 1e9
+    except Exception:  # noqa: BLE001
+        mem_gb = None
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"host_cores": cores, "usable_cores": usable, "cpu_model": model,
+            "mem_available_gb": mem_gb}
+
+
+def _cpu_workers(args, gb_per_worker=0.0):
+    """All usable host cores (the reference's workers='auto'), bounded only by
+    RAM when each worker holds `gb_per_worker` of scan lanes."""
+    if args.cpu_workers:
+        return args.cpu_workers
+    info = host_info()
+    w = info["usable_cores"]
+    if gb_per_worker and info["mem_available_gb"]:
+        w = min(w, max(1, int(0.6 * info["mem_available_gb"] / gb_per_worker)))
+    return max(1, w)
+
+
+# the reference's scan of one 64-query tile holds ~0.8 GB of (T, n, d_v) lanes at n = 16K
+def _lane_gb(n):
+    return 0.8 * n / 16384
+
+
 def cpu_baseline_sample(n, heads, batch, tiles, workers):
     """Reference CPU algorithm (oracle/scan_port.py = engine.scan_forward) on
     `tiles` whole 64-query tiles of the workload; returns (TFLOP/s, seconds,
@@ -179,12 +249,12 @@ def cpu_baseline_sample(n, heads, batch, tiles, workers):
 
 def cpu_full_configs(workers):
     """the reference CPU algorithm timed in full on the small
-    BASELINE configs (C1, C2 and C3 at n = 1K), on the same host threads."""
+    BASELINE configs (C1, C2 and C3 at n = 1K and 2K), on all host threads."""
     import oracle
 
     rows = []
     for name, (B, H, n) in (("C1", (1, 1, 1024)), ("C2 BERT-base", (8, 12, 512)),
-                            ("C3 n=1K", (1, 16, 1024))):
+                            ("C3 n=1K", (1, 16, 1024)), ("C3 n=2K", (1, 16, 2048))):
         Q, K, V = oracle.generate(0, "regular", b=B, h=H, n=n, d=64, d_v=64, dtype=np.float32)
         t0 = time.perf_counter()
         oracle.scan_forward_port(Q, K, V, block_size=128, tile_q=64, workers=workers)
@@ -195,20 +265,14 @@ def cpu_full_configs(workers):
     return rows
 
 
-def _cpu_workers(args):
-    cores = os.cpu_count() or 1
-    # each worker holds ~0.8 GB of (T, n, d_v) scan lanes at n = 16K; bound RAM
-    return args.cpu_workers or max(1, min(cores, 16))
-
-
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    workers = _cpu_workers(args)
-    tiles = args.cpu_sample_tiles or workers
     n, H, B = args.n, args.heads, args.batch
+    workers = _cpu_workers(args, _lane_gb(n))
+    tiles = args.cpu_sample_tiles or workers
     for _ in range(args.warmup):
         cpu_baseline_sample(min(n, 2048), 1, 1, 1, 1)
     vals, secs = [], []
@@ -223,12 +287,13 @@ def run_reference(args):
         "impl": "reference",
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (scanattn regular generator, seed 0)",
         "config": {"workload": f"C3 FP32 attention B{B} H{H} n{n} d64 (bounded CPU sample)",
                    "B": B, "H": H, "n": n, "d": 64, "dv": 64},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": workers, "kind": "port",
-                         "sample": desc, "sample_seconds_median": float(np.median(secs))},
+                         "sample": desc, "sample_seconds_median": float(np.median(secs)),
+                         **host_info()},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -236,333 +301,512 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- GPU arm
+class Ctx:
+    """Rank / device / process-group plumbing shared by the timed sections."""
+
+    def __init__(self, args):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        if self.world > 1 or args.dist_path:
+            # NCCL's communicator-init lines (ranks, NVLink/NVLS topology) go to a
+            # per-rank file (set before NCCL is loaded) and are echoed to stderr:
+            # the evidence that N ranks formed one communicator (stdout stays
+            # one JSON line)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/elsa_nccl.{os.getpid()}.log")
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        self.distributed = self.world > 1 or args.dist_path
+        self.comm = None
+        if self.distributed:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", str(self.world))
+            dist.init_process_group("nccl", device_id=self.dev)
+            t = torch.ones(1, device=self.dev)
+            dist.all_reduce(t)
+            torch.cuda.synchronize()
+            self.comm = self._nccl_lines(int(t.item()))
+        self.stream = torch.cuda.current_stream(self.dev)
+
+    def _nccl_lines(self, nranks_seen):
+        lines = []
+        for path in glob.glob(f"/tmp/elsa_nccl.{os.getpid()}.log*"):
+            try:
+                with open(path) as f:
+                    lines += [ln.rstrip() for ln in f]
+            except OSError:
+                pass
+        for ln in lines:
+            if "Init COMPLETE" in ln or "comm 0x" in ln or "NVLS" in ln or "P2P" in ln:
+                print(f"[rank {self.rank}] {ln}", file=sys.stderr)
+        version = next((ln.split("NCCL version", 1)[1].strip().split()[0]
+                        for ln in lines if "NCCL version" in ln), None)
+        complete = [ln for ln in lines if "Init COMPLETE" in ln]
+        nvls = any("NVLS" in ln and "enabled" in ln.lower() for ln in lines)
+        return {"backend": "nccl", "world": self.world, "all_reduce_ranks": nranks_seen,
+                "nccl_version": version, "init_complete_lines": len(complete),
+                "init_line": complete[0][-200:] if complete else None, "nvls_logged": nvls}
+
+    def barrier(self):
+        if self.distributed:
+            self.dist.barrier()
+
+    def max_over_ranks(self, x):
+        if not self.distributed:
+            return x
+        t = self.torch.tensor([float(x)], device=self.dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(self, x):
+        if not self.distributed:
+            return x
+        t = self.torch.tensor([float(x)], device=self.dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def timed(self, fn, steps):
+        """max-over-ranks ms per call of `fn` over `steps` calls: barrier +
+        synchronize on both sides, CUDA events on the launching stream."""
+        torch = self.torch
+        self.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(self.stream)
+        out = None
+        for _ in range(steps):
+            out = fn()
+        e1.record(self.stream)
+        torch.cuda.synchronize()
+        self.barrier()
+        return self.max_over_ranks(e0.elapsed_time(e1) / steps), out
+
+
+def sampled_parity(q, k, v, y_rows, row_lo, rows_wanted, seed):
+    """FP64 check of sampled output rows (oracles.py:92-98 restated in numpy:
+    row-max-stabilised softmax in float64). `y_rows` holds the flattened
+    (b, h, q) rows [row_lo, row_lo + len); returns the max per-row relative L2
+    error (verify.py:336-338) and the rows checked."""
+    import torch
+    B, H, n_q, d = q.shape
+    n_kv = k.shape[2]
+    total = y_rows.shape[0]
+    rng = np.random.default_rng(seed)
+    picks = sorted(set([0, total - 1] + rng.integers(0, total, max(rows_wanted - 2, 0)).tolist()))
+    by_head = {}
+    for p in picks:
+        bh, r = divmod(row_lo + p, n_q)
+        by_head.setdefault(bh, []).append((p, r))
+    sc = 1.0 / math.sqrt(d)
+    errs = []
+    for bh, items in by_head.items():
+        b, h = divmod(bh, H)
+        K = k[b, h].to(torch.float64).cpu().numpy()
+        V = v[b, h].to(torch.float64).cpu().numpy()
+        qs = q[b, h, [r for _, r in items]].to(torch.float64).cpu().numpy()
+        got = y_rows[[p for p, _ in items]].to(torch.float64).cpu().numpy()
+        s = (qs @ K.T) * sc
+        s -= s.max(axis=1, keepdims=True)
+        np.exp(s, out=s)
+        ref = (s @ V) / s.sum(axis=1, keepdims=True)
+        errs += list(np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1))
+        del K, V, s
+    return (max(errs) if errs else 0.0), len(errs)
+
+
+def _parity_block(ctx, err, rows, n_kv):
+    err = ctx.max_over_ranks(err)
+    rows = int(ctx.sum_over_ranks(rows))
+    thr = bound(n_kv)
+    return {"max_err": err, "bound": thr, "rows": rows, "pass": bool(err <= thr),
+            "oracle": "FP64 row-max-stabilised softmax on the host (oracles.py:92-98), "
+                      "per-row relative L2 (verify.py:336-338), bound u*L(n,128)*8 "
+                      "(verify.py:339-343)"}
+
+
+def headline(args, ctx, elsa, edist):
+    """The C3-16K step: N = 1 the single-GPU forward, N > 1 the B = N global
+    problem over (b, h, q) row slices (or KV-sharded with --shard kv)."""
+    torch = ctx.torch
+    world, rank, dev = ctx.world, ctx.rank, ctx.dev
+    H, n = args.heads, args.n
+    Bg = args.batch * world if ctx.distributed and args.shard == "q" else args.batch
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234)
+    q = torch.randn(Bg, H, n, 64, device=dev, generator=gen)
+    k = torch.randn(Bg, H, n, 64, device=dev, generator=gen)
+    v = torch.randn(Bg, H, n, 64, device=dev, generator=gen)
+    launches = [0]
+    chunks = edist.DEFAULT_CHUNKS if world <= 8 and 8 % world == 0 else world
+    state = {}
+
+    if not ctx.distributed:
+        def step():
+            y = elsa.scaled_dot_product_attention(q, k, v)
+            launches[0] += elsa.last_launch_count()
+            return 0, y.reshape(-1, 64)
+    elif args.shard == "q":
+        def step():
+            lo, y = edist.query_sharded_attention(q, k, v)
+            launches[0] += edist.last_launch_count()
+            return lo, y
+    else:
+        k_loc, v_loc, off = edist.shard_kv(k, v, rank, world, chunks)
+        k_loc, v_loc = k_loc.contiguous(), v_loc.contiguous()
+        state["kv"] = (k_loc, v_loc, off)
+
+        def step():
+            r = edist.kv_sharded_attention(q, k_loc, v_loc, off, n, chunks=chunks, gather=False,
+                                           exchange=args.exchange)
+            launches[0] += edist.last_launch_count()
+            return r
+
+    warm = max(args.warmup, 3)
+    for _ in range(warm):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(ctx.local)
+    clocks.start()
+    time.sleep(0.15)
+    launches[0] = 0
+    ms, (lo, y_rows) = ctx.timed(step, args.steps)
+    clock_info = clocks.stop()
+    timed_launches = launches[0]
+    fl = flops(Bg, H, n, n)
+    value = fl / (ms * 1e-3) / 1e12
+    parity = None
+    if not args.no_parity:
+        err, cnt = sampled_parity(q, k, v, y_rows, lo, max(8, 64 // world), seed=rank + 1)
+        parity = _parity_block(ctx, err, cnt, n)
+    plan = elsa.describe_plan(q[:1], k[:1], v[:1])
+    return dict(q=q, k=k, v=v, Bg=Bg, fl=fl, ms=ms, value=value, clocks=clock_info,
+                launches=timed_launches, parity=parity, plan=plan, chunks=chunks,
+                warmup=warm, state=state)
+
+
+def strong_c3(args, ctx, elsa, edist, hl):
+    """N > 1: the fixed B1 H16 n16K problem over the ranks' row slices."""
+    q, k, v = (t[:1] for t in (hl["q"], hl["k"], hl["v"]))
+    for _ in range(2):
+        edist.query_sharded_attention(q, k, v)
+    ms, _ = ctx.timed(lambda: edist.query_sharded_attention(q, k, v), max(3, args.steps // 2))
+    fl = flops(1, args.heads, args.n, args.n)
+    return {"workload": f"C3 B1 H{args.heads} n{args.n} d64 (fixed), (b, h, q) row slices over "
+                        f"{ctx.world} GPUs", "ms_per_step": ms,
+            "value": fl / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "scaling": "strong"}
+
+
+def e2e_block(args, ctx, elsa, hl):
+    """Each rank: its rows' Q/K/V from pinned host memory -> GPU -> Y rows back
+    to pinned host memory, through attention_from_host (C-ABI
+    elsa_fwd_f32_host, pipelined per head group); N > 1: the rank's own batch
+    elements (its row slice of the B = N problem)."""
+    torch = ctx.torch
+    q, k, v = hl["q"], hl["k"], hl["v"]
+    if ctx.distributed and args.shard == "q":
+        b0 = ctx.rank * args.batch
+        q, k, v = (t[b0:b0 + args.batch] for t in (q, k, v))
+    elif ctx.distributed:
+        return None  # the KV-sharded headline has no host-buffer entry
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    hy = torch.empty(tuple(q.shape[:-1]) + (64,), dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        elsa.attention_from_host(hq, hk, hv, out=hy, sync=False)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    steps_e2e = max(3, min(args.steps, 10))
+    ms, _ = ctx.timed(e2e_step, steps_e2e)
+    fl = hl["fl"]
+    h2d = ctx.sum_over_ranks((hq.numel() + hk.numel() + hv.numel()) * 4)
+    d2h = ctx.sum_over_ranks(hy.numel() * 4)
+    return {"value": fl / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps_e2e,
+            "api": "paper_2604_23798_b200.attention_from_host -> elsa_fwd_f32_host (C-ABI), "
+                   "pinned host buffers" + (", each rank its own batch elements (bytes summed "
+                                            "over ranks, max-over-ranks time)"
+                                            if ctx.distributed else "")}
+
+
+LONG = {"c4": ("C4", 1, 16, 65536), "c5": ("C5", 1, 8, 1 << 20)}
+
+
+def long_context(args, ctx, elsa, edist, spec_peak):
+    """C4 / C5 at this N: the single-GPU forward at N = 1, KV-sharded over the
+    ranks at N > 1 (strong scaling of the fixed problem)."""
+    torch = ctx.torch
+    out = []
+    names = [x.strip() for x in args.long.split(",") if x.strip() and x.strip() != "none"]
+    for key in names:
+        tag, B, H, n = LONG[key]
+        gen = torch.Generator(device=ctx.dev)
+        gen.manual_seed(64 + n % 977)
+        q = torch.randn(B, H, n, 64, device=ctx.dev, generator=gen)
+        k = torch.randn(B, H, n, 64, device=ctx.dev, generator=gen)
+        v = torch.randn(B, H, n, 64, device=ctx.dev, generator=gen)
+        fl = flops(B, H, n, n)
+        steps = 3 if key == "c4" else 1
+        launches = [0]
+        row = {"config": tag, "workload": f"{tag} FP32 attention B{B} H{H} n{n} d64 dv64",
+               "n_gpus": ctx.world, "scaling": "strong"}
+        if not ctx.distributed:
+            def step():
+                y = elsa.scaled_dot_product_attention(q, k, v)
+                launches[0] += elsa.last_launch_count()
+                return 0, y.reshape(-1, 64)
+            # C5 at N = 1 is a ~39 s step: warm it on the first 8192 query rows
+            # (same keys, same kernel); C4 warms on the full problem
+            if key == "c5":
+                elsa.scaled_dot_product_attention(q[:, :, :8192], k, v)
+            else:
+                step()
+            row["path"] = "single GPU: elsa_fwd_f32 (" + elsa.describe_plan(q, k, v) + ")"
+        else:
+            chunks = edist.DEFAULT_CHUNKS if ctx.world <= 8 and 8 % ctx.world == 0 else ctx.world
+            kl, vl, off = edist.shard_kv(k, v, ctx.rank, ctx.world, chunks)
+            kl, vl = kl.contiguous(), vl.contiguous()
+            ex = [args.exchange]
+
+            def step():
+                r = edist.kv_sharded_attention(q, kl, vl, off, n, chunks=chunks, gather=False,
+                                               exchange=ex[0])
+                launches[0] += edist.last_launch_count()
+                return r
+            step()  # full warm-up: rendezvous of the peer buffer, workspaces
+            row["path"] = (f"KV-sharded: {chunks} global key chunks, {chunks // ctx.world} per "
+                           f"rank, exchange={args.exchange}")
+            row["per_rank_keys"] = int(kl.shape[2])
+        torch.cuda.synchronize()
+        launches[0] = 0
+        ms, (lo, y_rows) = ctx.timed(step, steps)
+        tf = fl / (ms * 1e-3) / 1e12
+        row.update({"steps": steps, "ms_per_step": ms, "value": tf, "unit": "TFLOP/s",
+                    "gpu_launches_per_step": ctx.max_over_ranks(launches[0]) / steps,
+                    "frac_ffma_peak_per_gpu": tf / (ctx.world * spec_peak)})
+        if not args.no_parity:
+            err, cnt = sampled_parity(q, k, v, y_rows, lo, 8 if key == "c5" else 16,
+                                      seed=100 + ctx.rank)
+            row["parity"] = _parity_block(ctx, err, cnt, n)
+        out.append(row)
+        del q, k, v, y_rows
+        if ctx.distributed:
+            del kl, vl
+            edist.release_peer_buffers()
+        torch.cuda.empty_cache()
+    return out
+
+
+def sweep_block(args, ctx, elsa, hl, spec_peak):
+    """N = 1 kernel-only sweep: CUDA-graph replays, L2 flushed between them."""
+    torch, dev, stream = ctx.torch, ctx.dev, ctx.stream
+    q, k, v = hl["q"], hl["k"], hl["v"]
+    B, H, n = q.shape[0], q.shape[1], q.shape[2]
+    fl = hl["fl"]
+    sweep = []
+    flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
+    cases = [(1, 16, nn) for nn in (1024, 2048, 4096, 8192, 16384)] + [(8, 12, 512), (1, 1, 1024)]
+    for (bb, hh, nn) in cases:
+        qq = torch.randn(bb, hh, nn, 64, device=dev)
+        kk = torch.randn(bb, hh, nn, 64, device=dev)
+        vv = torch.randn(bb, hh, nn, 64, device=dev)
+        for _ in range(3):
+            elsa.scaled_dot_product_attention(qq, kk, vv)
+        torch.cuda.synchronize()
+        # capture one call so host-side Python overhead stays out of the
+        # measurement; replays are enqueued back to back (no host idle gaps)
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(dev)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                elsa.scaled_dot_product_attention(qq, kk, vv)
+        torch.cuda.synchronize()
+        reps = 30 if nn <= 4096 else 8
+        evs = []
+        for _ in range(reps):
+            flush.fill_(1.0)
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            graph.replay()
+            s1.record(stream)
+            evs.append((s0, s1))
+        torch.cuda.synchronize()
+        times = [a.elapsed_time(b) for a, b in evs[2:]]
+        t_ms = float(np.median(times))
+        tf = flops(bb, hh, nn, nn) / (t_ms * 1e-3) / 1e12
+        sweep.append({"B": bb, "H": hh, "n": nn, "ms": t_ms, "tflops": tf,
+                      "frac_ffma_peak": tf / spec_peak,
+                      "plan": elsa.describe_plan(qq, kk, vv)})
+        del qq, kk, vv, graph
+    # GPU comparator on the same box: torch SDPA FP32 (TF32 off), the paper's ME-SDPA
+    try:
+        torch.backends.cuda.matmul.allow_tf32 = False
+        torch.backends.cudnn.allow_tf32 = False
+        for _ in range(2):
+            torch.nn.functional.scaled_dot_product_attention(q, k, v)
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(3):
+            torch.nn.functional.scaled_dot_product_attention(q, k, v)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        tms = s0.elapsed_time(s1) / 3
+        sweep.append({"comparator": "torch.nn.functional.scaled_dot_product_attention fp32",
+                      "B": B, "H": H, "n": n, "ms": tms, "tflops": fl / (tms * 1e-3) / 1e12})
+    except Exception as exc:  # noqa: BLE001
+        sweep.append({"comparator": "torch sdpa fp32", "error": str(exc)[:200]})
+    # the FP16/BF16 variant (K5, tcgen05) on the same problem, for comparison
+    # (BASELINE configs[4]); flops 4*B*H*n^2*64, same as the FP32 count
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(16)
+    for dt, nm, dh in ((torch.bfloat16, "bf16", 64), (torch.float16, "fp16", 64),
+                       (torch.bfloat16, "bf16", 128)):
+        try:
+            if dh == 64:
+                q16, k16, v16 = q.to(dt), k.to(dt), v.to(dt)
+            else:  # wider heads (d = dv = 128), same sequence shape
+                q16, k16, v16 = (torch.randn(B, H, n, dh, device=dev, generator=gen).to(dt)
+                                 for _ in range(3))
+            fl16 = 4.0 * B * H * n * n * dh
+            row = {"variant": f"elsa {nm} (tcgen05)", "B": B, "H": H, "n": n, "d": dh}
+            for label, fn in (("elsa", lambda: elsa.scaled_dot_product_attention(q16, k16, v16)),
+                              ("torch", lambda: torch.nn.functional.scaled_dot_product_attention(
+                                  q16, k16, v16))):
+                for _ in range(2):
+                    fn()
+                s0 = torch.cuda.Event(enable_timing=True)
+                s1 = torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                for _ in range(5):
+                    fn()
+                s1.record(stream)
+                torch.cuda.synchronize()
+                tms = s0.elapsed_time(s1) / 5
+                row[f"{label}_ms"] = tms
+                row[f"{label}_tflops"] = fl16 / (tms * 1e-3) / 1e12
+            sweep.append(row)
+            del q16, k16, v16
+        except Exception as exc:  # noqa: BLE001
+            sweep.append({"variant": f"elsa {nm}", "error": str(exc)[:200]})
+    del flush
+    return sweep
+
+
 def main():
     args = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args)
         return
 
-    import torch
-    import torch.distributed as dist
-
+    ctx = Ctx(args)
+    torch = ctx.torch
     import paper_2604_23798_b200 as elsa
     from paper_2604_23798_b200 import dist as edist
 
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1 or args.dist_path:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29533")
-        os.environ.setdefault("RANK", "0")
-        os.environ.setdefault("WORLD_SIZE", str(world))
-        dist.init_process_group("nccl", device_id=dev)
-    sharded = world > 1 or args.dist_path
-    B, H, n = args.batch, args.heads, args.n
-    fl = flops(B, H, n, n)
-    stream = torch.cuda.current_stream(dev)
-
-    # ---- inputs (same generator as the reference, tensorio.py:177-195) ----
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234)
-    q = torch.randn(B, H, n, 64, device=dev, generator=gen)
-    k = torch.randn(B, H, n, 64, device=dev, generator=gen)
-    v = torch.randn(B, H, n, 64, device=dev, generator=gen)
-    chunks = 8 if world <= 8 and 8 % world == 0 else world
-    if sharded:
-        k_loc, v_loc, off = edist.shard_kv(k, v, rank, world, chunks)
-        k_loc, v_loc = k_loc.contiguous(), v_loc.contiguous()
-
-    launches = [0]
-    exchange = [args.exchange]
-
-    def step():
-        if not sharded:
-            y = elsa.scaled_dot_product_attention(q, k, v)
-            launches[0] += elsa.last_launch_count()
-            return y
-        if args.shard == "q":
-            r = edist.query_sharded_attention(q, k, v)
-        else:
-            r = edist.kv_sharded_attention(q, k_loc, v_loc, off, n, chunks=chunks, gather=False,
-                                           exchange=exchange[0])
-        launches[0] += 2 * (chunks // world) + 1
-        return r
-
-    if sharded and args.shard == "kv" and exchange[0] == "peer":
-        # the symmetric-memory rendezvous needs peer access between every pair
-        # of GPUs; if this node cannot provide it, measure the NCCL exchange
-        try:
-            step()
-            torch.cuda.synchronize()
-            ok = torch.ones(1, device=dev)
-        except Exception as exc:  # noqa: BLE001
-            print(f"[bench] peer exchange unavailable ({str(exc)[:120]}); using NCCL",
-                  file=sys.stderr)
-            ok = torch.zeros(1, device=dev)
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if ok.item() < 1:
-            exchange[0] = "nccl"
-
-    def barrier():
-        if sharded:
-            dist.barrier()
-
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.15)
-    launches[0] = 0
-    barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    ms_total = e0.elapsed_time(e1)
-    clock_info = clocks.stop()
-    timed_launches = launches[0]
-    if sharded:
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
-    ms = ms_total / args.steps
-    value = fl / (ms * 1e-3) / 1e12
-
-    # ---- e2e through the public API with pinned host buffers ----
-    e2e = None
-    if not args.no_e2e and sharded:
-        # each rank: H2D of Q and its K/V shard, the KV-sharded forward, D2H of
-        # its Y row slice (the ranks' slices together are the whole Y)
-        k_src, v_src = (k, v) if args.shard == "q" else (k_loc, v_loc)
-        hq = q.cpu().pin_memory()
-        hk, hv = k_src.cpu().pin_memory(), v_src.cpu().pin_memory()
-        dq, dk, dv_ = torch.empty_like(q), torch.empty_like(k_src), torch.empty_like(v_src)
-        hy = [None]
-
-        def e2e_step_dist():
-            dq.copy_(hq, non_blocking=True)
-            dk.copy_(hk, non_blocking=True)
-            dv_.copy_(hv, non_blocking=True)
-            if args.shard == "q":
-                _, yr = edist.query_sharded_attention(dq, dk, dv_)
-            else:
-                _, yr = edist.kv_sharded_attention(dq, dk, dv_, off, n, chunks=chunks,
-                                                   gather=False, exchange=exchange[0])
-            if hy[0] is None:
-                hy[0] = torch.empty(yr.shape, dtype=yr.dtype).pin_memory()
-            hy[0].copy_(yr, non_blocking=True)
-
-        for _ in range(2):
-            e2e_step_dist()
-        torch.cuda.synchronize()
-        barrier()
-        steps_e2e = max(3, min(args.steps, 10))
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(steps_e2e):
-            e2e_step_dist()
-        a1.record(stream)
-        torch.cuda.synchronize()
-        t = torch.tensor([a0.elapsed_time(a1) / steps_e2e], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-        e2e = {"value": fl / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": (q.numel() + k_src.numel() + v_src.numel()) * 4 * world,
-               "d2h_bytes_per_step": hy[0].numel() * 4 * world, "steps": steps_e2e,
-               "api": "paper_2604_23798_b200.dist.kv_sharded_attention per rank, pinned host "
-                      "buffers (bytes summed over ranks; max-over-ranks time)"}
-    if not args.no_e2e and not sharded:
-        hq = q.cpu().pin_memory()
-        hk = k.cpu().pin_memory()
-        hv = v.cpu().pin_memory()
-        hy = torch.empty((B, H, n, 64), dtype=torch.float32).pin_memory()
-
-        def e2e_step():
-            # the public host-buffer entry point (elsa_fwd_f32_host): per-head-group
-            # H2D -> forward -> D2H pipelined on internal streams; the current
-            # stream waits for the last D2H
-            elsa.attention_from_host(hq, hk, hv, out=hy, sync=False)
-
-        for _ in range(2):
-            e2e_step()
-        torch.cuda.synchronize()
-        steps_e2e = max(3, min(args.steps, 10))
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(steps_e2e):
-            e2e_step()
-        a1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = a0.elapsed_time(a1) / steps_e2e
-        e2e = {"value": fl / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 3 * q.numel() * 4, "d2h_bytes_per_step": hy.numel() * 4,
-               "steps": steps_e2e,
-               "api": "paper_2604_23798_b200.attention_from_host -> elsa_fwd_f32_host (C-ABI), "
-                      "pinned host buffers"}
-
-    # ---- roofline: FFMA peak (spec clock) and the K4 microbenchmark ----
+    world, rank = ctx.world, ctx.rank
     peaks = measured_peaks()
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
     spec_peak = SMS * FFMA_LANES * 2 * fmax * 1e6 / 1e12
+
+    hl = headline(args, ctx, elsa, edist)
+    strong = None
+    if ctx.distributed and args.shard == "q" and world > 1:
+        strong = strong_c3(args, ctx, elsa, edist, hl)
+    e2e = None if args.no_e2e else e2e_block(args, ctx, elsa, hl)
+
+    # ---- roofline: FFMA peak (spec clock) and the K4 microbenchmark ----
     k4 = None
     try:
-        k4 = elsa.ffma_peak_tflops(dev)
+        k4 = elsa.ffma_peak_tflops(ctx.dev)
     except Exception:  # noqa: BLE001
         k4 = None
+    per_gpu = hl["value"] / world
     traffic, traffic_workload = ncu_traffic()
+    B1 = args.batch
     roofline = {
-        "bound": "ffma", "achieved": value, "peak": spec_peak, "unit": "TFLOP/s",
-        "frac": value / spec_peak,
+        "bound": "ffma", "achieved": per_gpu, "peak": spec_peak, "unit": "TFLOP/s",
+        "frac": per_gpu / spec_peak,
         "peak_source": f"148 SM x 128 FP32 lanes x 2 x {fmax:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-        "k4_ffma_measured": k4, "frac_of_k4": (value / k4) if k4 else None,
+        "k4_ffma_measured": k4, "frac_of_k4": (per_gpu / k4) if k4 else None,
         "traffic": traffic, "traffic_workload": traffic_workload,
-        "algorithmic_bytes_per_launch": 4 * B * H * (n * 64 * 3 + n * 64),
-        "kernel": "elsa::fwd_f32_kernel (" + elsa.describe_plan(q, k, v) + ")" if not sharded else "elsa::fwd_f32_kernel",
-        "measurement": "CUDA events on the launching stream around the K timed steps; "
-                       "one kernel launch per step at this shape",
+        "algorithmic_flops_per_launch": flops(B1, args.heads, args.n, args.n),
+        "algorithmic_bytes_per_launch": 4 * B1 * args.heads * (args.n * 64 * 3 + args.n * 64),
+        "kernel": "elsa::fwd_f32_kernel (" + hl["plan"] + ")",
+        "measurement": "CUDA events on the launching stream around the K timed steps (max over "
+                       "ranks); one kernel launch per GPU per step at this shape",
     }
 
-    # ---- sweep (kernel-only: CUDA-graph replays, L2 flushed between them) ----
     sweep = []
-    if not args.no_sweep and not sharded:
-        flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)
-        cases = [(1, 16, nn) for nn in (1024, 2048, 4096, 8192, 16384)] + [(8, 12, 512), (1, 1, 1024)]
-        for (bb, hh, nn) in cases:
-            qq = torch.randn(bb, hh, nn, 64, device=dev)
-            kk = torch.randn(bb, hh, nn, 64, device=dev)
-            vv = torch.randn(bb, hh, nn, 64, device=dev)
-            for _ in range(3):
-                elsa.scaled_dot_product_attention(qq, kk, vv)
-            torch.cuda.synchronize()
-            # capture one call so host-side Python overhead stays out of the
-            # measurement; replays are enqueued back to back (no host idle gaps)
-            graph = torch.cuda.CUDAGraph()
-            cap = torch.cuda.Stream(dev)
-            with torch.cuda.stream(cap):
-                with torch.cuda.graph(graph, stream=cap):
-                    elsa.scaled_dot_product_attention(qq, kk, vv)
-            torch.cuda.synchronize()
-            reps = 30 if nn <= 4096 else 8
-            evs = []
-            for _ in range(reps):
-                flush.fill_(1.0)
-                s0 = torch.cuda.Event(enable_timing=True)
-                s1 = torch.cuda.Event(enable_timing=True)
-                s0.record(stream)
-                graph.replay()
-                s1.record(stream)
-                evs.append((s0, s1))
-            torch.cuda.synchronize()
-            times = [a.elapsed_time(b) for a, b in evs[2:]]
-            t_ms = float(np.median(times))
-            tf = flops(bb, hh, nn, nn) / (t_ms * 1e-3) / 1e12
-            sweep.append({"B": bb, "H": hh, "n": nn, "ms": t_ms, "tflops": tf,
-                          "frac_ffma_peak": tf / spec_peak,
-                          "plan": elsa.describe_plan(qq, kk, vv)})
-            del qq, kk, vv, graph
-        # GPU comparator on the same box: torch SDPA FP32 (TF32 off), the paper's ME-SDPA
-        try:
-            torch.backends.cuda.matmul.allow_tf32 = False
-            torch.backends.cudnn.allow_tf32 = False
-            for _ in range(2):
-                torch.nn.functional.scaled_dot_product_attention(q, k, v)
-            s0 = torch.cuda.Event(enable_timing=True)
-            s1 = torch.cuda.Event(enable_timing=True)
-            s0.record(stream)
-            for _ in range(3):
-                torch.nn.functional.scaled_dot_product_attention(q, k, v)
-            s1.record(stream)
-            torch.cuda.synchronize()
-            tms = s0.elapsed_time(s1) / 3
-            sweep.append({"comparator": "torch.nn.functional.scaled_dot_product_attention fp32",
-                          "B": B, "H": H, "n": n, "ms": tms, "tflops": fl / (tms * 1e-3) / 1e12})
-        except Exception as exc:  # noqa: BLE001
-            sweep.append({"comparator": "torch sdpa fp32", "error": str(exc)[:200]})
-        # the FP16/BF16 variant (K5, tcgen05) on the same problem, for comparison
-        # (BASELINE configs[4]); flops 4*B*H*n^2*64, same as the FP32 count
-        for dt, nm, dh in ((torch.bfloat16, "bf16", 64), (torch.float16, "fp16", 64),
-                           (torch.bfloat16, "bf16", 128)):
-            try:
-                if dh == 64:
-                    q16, k16, v16 = q.to(dt), k.to(dt), v.to(dt)
-                else:  # wider heads (d = dv = 128), same sequence shape
-                    q16, k16, v16 = (torch.randn(B, H, n, dh, device=dev, generator=gen).to(dt)
-                                     for _ in range(3))
-                fl16 = 4.0 * B * H * n * n * dh
-                row = {"variant": f"elsa {nm} (tcgen05)", "B": B, "H": H, "n": n, "d": dh}
-                for label, fn in (("elsa", lambda: elsa.scaled_dot_product_attention(q16, k16, v16)),
-                                  ("torch", lambda: torch.nn.functional.scaled_dot_product_attention(
-                                      q16, k16, v16))):
-                    for _ in range(2):
-                        fn()
-                    s0 = torch.cuda.Event(enable_timing=True)
-                    s1 = torch.cuda.Event(enable_timing=True)
-                    s0.record(stream)
-                    for _ in range(5):
-                        fn()
-                    s1.record(stream)
-                    torch.cuda.synchronize()
-                    tms = s0.elapsed_time(s1) / 5
-                    row[f"{label}_ms"] = tms
-                    row[f"{label}_tflops"] = fl16 / (tms * 1e-3) / 1e12
-                sweep.append(row)
-                del q16, k16, v16
-            except Exception as exc:  # noqa: BLE001
-                sweep.append({"variant": f"elsa {nm}", "error": str(exc)[:200]})
+    if not args.no_sweep and not ctx.distributed:
+        sweep = sweep_block(args, ctx, elsa, hl, spec_peak)
+
+    # free the headline tensors before the long-context problems (C5: 8 GiB)
+    q_shape = tuple(hl["q"].shape)
+    for key in ("q", "k", "v"):
+        hl.pop(key)
+    hl["state"].clear()
+    torch.cuda.empty_cache()
+    longc = long_context(args, ctx, elsa, edist, spec_peak)
 
     # ---- CPU baseline: the reference's algorithm on the host cores (rank 0, N=1) ----
     cpu = None
-    if rank == 0 and not sharded and not args.no_cpu_baseline:
-        workers = _cpu_workers(args)
+    if rank == 0 and not ctx.distributed and not args.no_cpu_baseline:
+        n, H, B = args.n, args.heads, args.batch
+        workers = _cpu_workers(args, _lane_gb(n))
         tiles = args.cpu_sample_tiles or workers
         val, secs, desc = cpu_baseline_sample(n, H, B, tiles, workers)
+        full_workers = _cpu_workers(args, _lane_gb(2048))
         cpu = {"value": val, "unit": "TFLOP/s", "cores": workers, "kind": "port",
-               "sample": desc, "seconds": secs,
-               "full_small_configs": cpu_full_configs(workers)}
+               "sample": desc, "seconds": secs, **host_info(),
+               "full_small_configs": cpu_full_configs(full_workers)}
 
-    if sharded and args.shard == "kv":
-        # per-rank working set of one step: all of Q, this rank's K/V shard and
-        # its chunk states (m, S, W for every query row)
-        per = chunks // world
-        ws_mb = (q.numel() + k_loc.numel() + v_loc.numel()
-                 + per * B * H * n * (2 + 64)) * 4 / 1e6
-        l2_note = ("per-rank step working set %.0f MB (Q, K/V shard, chunk states) > 126 MB L2; "
-                   "sweep flushes L2 (256 MB write) between timed iterations" % ws_mb)
-    else:
-        l2_note = ("inputs 3x%.0f MB > 126 MB L2; sweep flushes L2 (256 MB write) "
-                   "between timed iterations" % (q.numel() * 4 / 1e6))
+    Bg = hl["Bg"]
     if rank == 0:
+        if ctx.distributed and args.shard == "q":
+            workload = (f"C3 FP32 attention B{Bg} H{args.heads} n{args.n} d64 dv64: one "
+                        f"B{args.batch} H{args.heads} n{args.n} problem per GPU, (b, h, q) row "
+                        f"slices, no exchange")
+            par = f"batch x heads row slices over {world} GPUs (query-sharded)"
+        elif ctx.distributed:
+            workload = (f"C3 FP32 attention B{Bg} H{args.heads} n{args.n} d64 dv64, KV-sharded "
+                        f"over {world} GPUs ({hl['chunks']} chunks)")
+            par = f"kv-shard{world}"
+        else:
+            workload = f"C3 FP32 attention B{Bg} H{args.heads} n{args.n} d64 dv64"
+            par = "single GPU"
         line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "metric": METRIC, "value": hl["value"], "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": hl["warmup"], "ms_per_step": hl["ms"],
+            "higher_is_better": True,
+            "scaling": "weak" if (ctx.distributed and args.shard == "q") or world == 1
+                       else "strong",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic N(0,1) Q/K/V (torch.randn), resident in HBM",
-            "config": {"workload": f"C3 FP32 attention B{B} H{H} n{n} d64 dv64"
-                                   + (f", KV-sharded over {world} GPUs ({chunks} chunks)"
-                                      if sharded else ""),
-                       "B": B, "H": H, "n": n, "d": 64, "dv": 64,
-                       "l2": l2_note,
-                       "parallelism": f"kv-shard{world}" if sharded else "single GPU",
-                       "exchange": (exchange[0] if args.shard == "kv" else "none (query-sharded)")
-                                   if sharded else None},
-            "e2e": e2e, "gpu_launches": timed_launches, "clocks": clock_info,
-            "roofline": roofline, "cpu_baseline": cpu, "sweep": sweep,
+            "config": {"workload": workload, "B": Bg, "H": args.heads, "n": args.n, "d": 64,
+                       "dv": 64, "shape": list(q_shape),
+                       "l2": "inputs 3x%.0f MB per GPU > 126 MB L2 (no L2 reuse across steps); "
+                             "the sweep flushes L2 (256 MB write) between timed iterations"
+                             % (args.batch * args.heads * args.n * 64 * 4 / 1e6),
+                       "parallelism": par},
+            "parity": hl["parity"],
+            "e2e": e2e, "gpu_launches": hl["launches"], "clocks": hl["clocks"],
+            "roofline": roofline, "strong": strong, "long_context": longc, "comm": ctx.comm,
+            "cpu_baseline": cpu, "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
-    if sharded:
-        dist.destroy_process_group()
+    if ctx.distributed:
+        ctx.dist.destroy_process_group()
 
 
 if __name__ == "__main__":

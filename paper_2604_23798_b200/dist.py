@@ -43,9 +43,26 @@ import torch.distributed as dist
 from .errors import ShapeError
 
 __all__ = ["chunk_bounds", "owned_chunks", "row_slices", "kv_sharded_attention",
-           "query_sharded_attention", "shard_kv", "DEFAULT_CHUNKS"]
+           "query_sharded_attention", "shard_kv", "release_peer_buffers", "last_launch_count",
+           "resolve_exchange",
+           "DEFAULT_CHUNKS"]
 
 DEFAULT_CHUNKS = 8
+
+
+_LAUNCHES = [0]
+
+
+def _tally():
+    """Add the kernels the last libelsa call launched to this call's count."""
+    from .attention import last_launch_count
+    _LAUNCHES[0] += last_launch_count()
+
+
+def last_launch_count():
+    """Kernels the last kv_sharded_attention / query_sharded_attention call
+    launched on this rank (libelsa kernels only; NCCL's are not counted)."""
+    return _LAUNCHES[0]
 
 
 def chunk_bounds(n_kv, chunks):
@@ -88,20 +105,34 @@ def _gpu_merge(m, S, W):
     return merge_states(m, S, W, finalize=True)
 
 
+# One symmetric state buffer per (device, group), grown on demand and reused
+# as a prefix for smaller shapes, so varying sequence lengths do not pile up
+# peer-mapped allocations (release_peer_buffers() frees them).
 _PEER_BUFS = {}
 
 
+def release_peer_buffers():
+    """Drop the cached symmetric-memory state buffers (call on every rank)."""
+    _PEER_BUFS.clear()
+
+
 def _peer_buffer(per, rows, dv, device, group):
-    """Symmetric state buffer [m | S | W] for (per, rows, dv), rendezvoused once
-    per shape and group and reused (the trailing barrier of every call keeps
-    reuse safe)."""
+    """Symmetric state buffer holding at least per*rows*(2+dv) floats,
+    rendezvoused on first use (and when a larger shape needs a bigger one) and
+    reused; the trailing barrier of every call keeps reuse safe. Every rank
+    runs the same shape sequence, so the collective rendezvous stays matched."""
+    import os
+    # only unicast peer pointers (buffer_ptrs) are read; the NVLS multicast
+    # object symmetric memory would also try to export is not needed
+    os.environ.setdefault("TORCH_SYMM_MEM_DISABLE_MULTICAST", "1")
     import torch.distributed._symmetric_memory as symm_mem
 
-    key = (per, rows, dv, device.index, id(group))
+    key = (device.index, id(group))
+    need = per * rows * (2 + dv)
     hit = _PEER_BUFS.get(key)
-    if hit is None:
-        n = per * rows * (2 + dv)
-        buf = symm_mem.empty(n, dtype=torch.float32, device=device)
+    if hit is None or hit[0].numel() < need:
+        _PEER_BUFS.pop(key, None)
+        buf = symm_mem.empty(need, dtype=torch.float32, device=device)
         grp = group if group is not None else dist.group.WORLD
         hdl = symm_mem.rendezvous(buf, grp)
         hit = (buf, hdl)
@@ -113,7 +144,7 @@ def _peer_exchange_merge(q, states_fn, per, rows, dv, chunks, group, rank, world
     buf, hdl = _peer_buffer(per, rows, dv, q.device, group)
     m = buf[: per * rows].view(per, rows)
     S = buf[per * rows: 2 * per * rows].view(per, rows)
-    W = buf[2 * per * rows:].view(per, rows, dv)
+    W = buf[2 * per * rows: per * rows * (2 + dv)].view(per, rows, dv)
     states_fn(m, S, W)
     hdl.barrier(channel=0)  # every rank's states written (device-side, stream-ordered)
     lo, hi = row_slices(rows, world)[rank]
@@ -123,13 +154,25 @@ def _peer_exchange_merge(q, states_fn, per, rows, dv, chunks, group, rank, world
     Wp = [b + 2 * per * rows * 4 for b in base]
     from .attention import merge_peer_states
     y_rows = merge_peer_states(mp, Sp, Wp, per, rows, lo, hi - lo, dv, device=q.device)
+    _tally()
     hdl.barrier(channel=1)  # peers finished reading before the buffer is rewritten
     return lo, y_rows
 
 
+def resolve_exchange(exchange, q, group=None, injected=False):
+    """``"auto"`` -> ``"peer"`` when the group runs NCCL on CUDA tensors and
+    the libelsa kernels do the compute, else ``"nccl"`` (the packed
+    all_to_all path, which also serves gloo / CPU and world size 1)."""
+    if exchange != "auto":
+        return exchange
+    use_peer = (not injected and q.is_cuda and dist.is_initialized()
+                and dist.get_backend(group) == "nccl")
+    return "peer" if use_peer else "nccl"
+
+
 def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
                          chunks=DEFAULT_CHUNKS, gather=True, partial_fn=None, merge_fn=None,
-                         exchange="nccl"):
+                         exchange="auto"):
     """Exact attention with keys sharded across the ranks of ``group``.
 
     ``q``: full (B, H, n_q, d) on this rank; ``k_local``/``v_local``: this
@@ -137,8 +180,14 @@ def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
     returned by :func:`shard_kv`); ``n_kv``: total key count. Returns the full
     Y (B, H, n_q, dv) when ``gather`` else ``(row_begin, Y_rows)`` for this
     rank's row slice (rows ordered (b, h, q)).
+
+    ``exchange``: ``"peer"`` (the fused symmetric-memory merge), ``"nccl"``
+    (all_to_all + K2) or ``"auto"`` (default): peer when the process group
+    runs the NCCL backend on CUDA tensors and no compute step is injected,
+    else nccl (which at world size 1 needs no process group at all).
     """
     injected = partial_fn is not None or merge_fn is not None
+    _LAUNCHES[0] = 0
     partial_fn = partial_fn or _gpu_partial
     merge_fn = merge_fn or _gpu_merge
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -152,6 +201,7 @@ def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
     if kv_offset != bounds[own[0]][0] or kv_offset + k_local.shape[2] != bounds[own[-1]][1]:
         raise ShapeError("local K/V rows do not match this rank's chunk range")
 
+    exchange = resolve_exchange(exchange, q, group, injected)
     if exchange == "peer":
         if injected:
             raise ShapeError("the peer exchange runs the libelsa kernels only")
@@ -164,6 +214,7 @@ def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
                 lo, hi = bounds[c]
                 partial_states(q, k_local, v_local, lo - kv_offset, hi - kv_offset, kv_splits=0,
                                out=(m[i], S[i], W[i]))
+                _tally()
 
         my_lo, y_rows = _peer_exchange_merge(q, states_fn, per, rows, dv, chunks, group, rank,
                                              world)
@@ -187,6 +238,8 @@ def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
     for i, c in enumerate(own):
         lo, hi = bounds[c]
         m, S, W = partial_fn(q, k_local, v_local, lo - kv_offset, hi - kv_offset)
+        if not injected:
+            _tally()
         states[i, :, 0] = m.reshape(rows)
         states[i, :, 1] = S.reshape(rows)
         states[i, :, 2:] = W.reshape(rows, dv)
@@ -210,6 +263,8 @@ def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
     # 3. fixed balanced tree over the C chunk states
     y_rows = merge_fn(allc[..., 0].contiguous(), allc[..., 1].contiguous(),
                       allc[..., 2:].contiguous())
+    if not injected:
+        _tally()
     if not gather:
         return my_lo, y_rows
     if world == 1:
@@ -224,12 +279,18 @@ def kv_sharded_attention(q, k_local, v_local, kv_offset, n_kv, group=None,
     return y.reshape(B, H, n_q, dv)
 
 
-def query_sharded_attention(q, k, v, group=None, gather=False):
-    """The control experiment of SURVEY §8e: rank r computes the query rows of
-    its slice (flattened (b, h, q) order, the same slices as the KV-sharded
-    path) against ALL keys — no exchange, no merge. Returns ``(row_begin,
-    Y_rows)``, or the full Y with ``gather``."""
-    from .attention import scaled_dot_product_attention
+def query_sharded_attention(q, k, v, group=None, gather=False, attn_fn=None):
+    """Batch x heads sharding (BASELINE north_star; SURVEY §8e's control
+    experiment): rank r computes the query rows of its slice (flattened
+    (b, h, q) order, the same slices as the KV-sharded path) against ALL keys
+    — no exchange, no merge. A slice that starts or ends inside a head runs
+    that head's partial query range; the whole heads between run as one
+    launch. Returns ``(row_begin, Y_rows)``, or the full Y with ``gather``.
+    ``attn_fn(q, k, v) -> y`` (default: the libelsa forward) is injectable so
+    the slicing is testable on CPU."""
+    injected = attn_fn is not None
+    if attn_fn is None:
+        from .attention import scaled_dot_product_attention as attn_fn
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -238,6 +299,7 @@ def query_sharded_attention(q, k, v, group=None, gather=False):
     rows = B * H * n_q
     slices = row_slices(rows, world)
     lo, hi = slices[rank]
+    _LAUNCHES[0] = 0
     # the slice = [partial head] + whole heads (one launch) + [partial head]
     qf, kf, vf = (t.reshape(B * H, 1, t.shape[2], t.shape[3]) for t in (q, k, v))
     out = torch.empty((hi - lo, dv), device=q.device, dtype=torch.float32)
@@ -246,14 +308,17 @@ def query_sharded_attention(q, k, v, group=None, gather=False):
         bh, q0 = divmod(r, n_q)
         if q0 == 0 and hi - r >= n_q:  # a run of whole heads
             nh = (hi - r) // n_q
-            y = scaled_dot_product_attention(qf[bh:bh + nh].transpose(0, 1),
-                                             kf[bh:bh + nh].transpose(0, 1),
-                                             vf[bh:bh + nh].transpose(0, 1))
+            y = attn_fn(qf[bh:bh + nh].transpose(0, 1), kf[bh:bh + nh].transpose(0, 1),
+                        vf[bh:bh + nh].transpose(0, 1))
+            if not injected:
+                _tally()
             out[r - lo: r - lo + nh * n_q] = y.reshape(nh * n_q, dv)
             r += nh * n_q
         else:
             q1 = min(n_q, q0 + (hi - r))
-            y = scaled_dot_product_attention(qf[bh:bh + 1, :, q0:q1], kf[bh:bh + 1], vf[bh:bh + 1])
+            y = attn_fn(qf[bh:bh + 1, :, q0:q1], kf[bh:bh + 1], vf[bh:bh + 1])
+            if not injected:
+                _tally()
             out[r - lo: r - lo + (q1 - q0)] = y.reshape(q1 - q0, dv)
             r += q1 - q0
     if not gather:

@@ -39,7 +39,7 @@ def pg():
     yield dist.group.WORLD
     if created:
         torch.cuda.synchronize()
-        edist._PEER_BUFS.clear()
+        edist.release_peer_buffers()
         dist.destroy_process_group()
 
 

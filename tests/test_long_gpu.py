@@ -1,0 +1,107 @@
+"""C5 (BASELINE configs[4]: n = 2^20 keys, H = 8, d = dv = 64) in the GPU suite.
+
+All 2^20 keys and values per head, 256 query rows per head (the cost of the
+test is the key length, which is what C5 exercises: the per-CTA chain cap of
+1024 key tiles forces >= 16 key splits and the K2 tree over them). The gate is
+the reference's per-row bound u * L(2^20, 128) * 8 = 1.72e-5 (verify.py:339-343)
+against FP64 rows computed on the CPU by ``oracle.sampled_rows_fp64``
+(restating oracles.py:92-98). The KV-sharded path (Proposition 1,
+PAPER.md:662-666; C = 8 global chunks at world size 1, both exchanges) is
+gated the same way and must be bitwise equal between the exchanges.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+
+import paper_2604_23798_b200 as elsa  # noqa: E402
+from paper_2604_23798_b200 import dist as edist  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+N_KV = 1 << 20
+H = 8
+N_Q = 256
+HEADS = (0, 5)        # heads checked against FP64
+ROWS_PER_HEAD = 12
+
+
+@pytest.fixture(scope="module")
+def c5():
+    g = torch.Generator(device=DEV)
+    g.manual_seed(20)
+    q = torch.randn(1, H, N_Q, 64, device=DEV, generator=g)
+    k = torch.randn(1, H, N_KV, 64, device=DEV, generator=g)
+    v = torch.randn(1, H, N_KV, 64, device=DEV, generator=g)
+    # FP64 oracle rows for the checked heads (host copies made once)
+    rng = np.random.default_rng(5)
+    rows = sorted(set([0, N_Q - 1] + rng.integers(0, N_Q, ROWS_PER_HEAD).tolist()))
+    Q64 = q[:, list(HEADS)].double().cpu().numpy()
+    K64 = k[:, list(HEADS)].cpu().numpy().astype(np.float64)
+    V64 = v[:, list(HEADS)].cpu().numpy().astype(np.float64)
+    sel = [(0, j, r) for j in range(len(HEADS)) for r in rows]
+    ref = oracle.sampled_rows_fp64(Q64, K64, V64, sel)
+    del K64, V64
+    yield q, k, v, sel, ref
+    del q, k, v
+    torch.cuda.empty_cache()
+
+
+def _check(y, sel, ref, what):
+    got = np.stack([y[0, HEADS[j], r].double().cpu().numpy() for (_, j, r) in sel])
+    err = oracle.row_rel_err(got, ref)
+    thr = oracle.bound_threshold(N_KV)
+    assert thr == pytest.approx(2.0 ** -24 * 36 * 8)
+    assert err.max() <= thr, f"{what}: max sampled row err {err.max():.3e} > {thr:.3e}"
+    return float(err.max())
+
+
+def test_c5_direct_within_bound(c5):
+    q, k, v, sel, ref = c5
+    plan = elsa.describe_plan(q, k, v)
+    y = elsa.scaled_dot_product_attention(q, k, v, check_numerics=True)
+    _check(y, sel, ref, f"C5 direct ({plan})")
+    # the chain cap: 2^20 keys in 64-key tiles need >= 16 splits
+    assert elsa.resolve_kv_splits(q, k, v) >= 16
+    # deterministic
+    y2 = elsa.scaled_dot_product_attention(q, k, v)
+    assert torch.equal(y, y2)
+
+
+@pytest.fixture(scope="module")
+def pg():
+    created = False
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(DEV)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+        created = True
+    yield dist.group.WORLD
+    if created:
+        torch.cuda.synchronize()
+        edist.release_peer_buffers()
+        dist.destroy_process_group()
+
+
+def test_c5_kv_sharded_peer_and_nccl(c5, pg):
+    q, k, v, sel, ref = c5
+    kl, vl, off = edist.shard_kv(k, v, 0, 1, 8)
+    y_peer = edist.kv_sharded_attention(q, kl, vl, off, N_KV, chunks=8, exchange="peer")
+    y_nccl = edist.kv_sharded_attention(q, kl, vl, off, N_KV, chunks=8, exchange="nccl")
+    elsa.check_device_error(DEV)
+    assert torch.equal(y_peer, y_nccl)
+    _check(y_peer, sel, ref, "C5 kv-sharded (8 chunks)")
