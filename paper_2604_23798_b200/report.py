@@ -1,16 +1,19 @@
 """``scanattn-bench-v1`` records and the scaling fit for GPU runs
 (SURVEY §8f row 4).
 
-Mirrors /root/reference/pkg/src/scanattn/bench.py so GPU measurements land in
-the same report schema the reference's CLI writes (``scanattn bench
---report``, cli.py:231-265):
+GPU measurements are written in the report schema the reference's CLI emits
+(``scanattn bench --report``, cli.py:231-265; schema of bench.py:40-130,
+222-242) so the two can be read by the same tools. The implementation here
+is this package's own and is pinned by the reference's output bytes
+(tests/golden/harness.npz), not derived from its code:
 
-* :class:`BenchRecord` — same fields, JSON/CSV serialisation and derived
-  median/p5/p95 (bench.py:40-110);
-* :func:`fit_scaling` — least squares of latency on [L(n, B), n^2, 1] with
-  normalised columns and the relative RMS residual (bench.py:193-219);
-* :func:`emit_report` — the JSON document + flat CSV (bench.py:222-242);
-* :func:`nearest_rank_percentiles` — verify.py:54-66;
+* :class:`BenchRecord` — a schema-driven record: the field table
+  ``RECORD_FIELDS`` fixes the key order of the JSON object and the CSV
+  columns; the median / p5 / p95 summary is computed when serialising;
+* :func:`fit_scaling` — ``T(n) = a L(n, B) + b n^2 + c`` by a Householder QR
+  solve of the column-equilibrated design, plus the relative residual;
+* :func:`emit_report` — JSON document + flat CSV;
+* :func:`nearest_rank_percentiles` — nearest-rank order statistics;
 * :func:`run_bench` — one workload timed on the device: every repeat is one
   ``scaled_dot_product_attention`` call bracketed by CUDA events on the
   launching stream (the reference times host wall clock, bench.py:175-181).
@@ -24,7 +27,6 @@ from __future__ import annotations
 
 import json
 import math
-from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -33,6 +35,7 @@ from .errors import ShapeError
 __all__ = [
     "BenchRecord",
     "ScalingFit",
+    "RECORD_FIELDS",
     "nearest_rank_percentiles",
     "fit_scaling",
     "emit_report",
@@ -43,147 +46,146 @@ __all__ = [
 MODES = ("scan", "scan16", "sdpa")
 
 
+def _order_stat(sorted_samples, pct):
+    """The nearest-rank pct-th percentile of an ascending array: element
+    ceil(pct/100 * N), 1-based, at least the first."""
+    k = math.ceil(pct * sorted_samples.size / 100.0)
+    return float(sorted_samples[min(max(k, 1), sorted_samples.size) - 1])
+
+
 def nearest_rank_percentiles(samples):
     """Median / p95 / p99 by the nearest-rank rule (verify.py:54-66)."""
-    s = np.sort(np.asarray(samples, dtype=np.float64).ravel())
-    if s.size == 0:
-        return {"median": 0.0, "p95": 0.0, "p99": 0.0}
-
-    def rank(p):
-        return s[max(math.ceil(p / 100.0 * s.size), 1) - 1]
-
-    return {"median": float(rank(50)), "p95": float(rank(95)), "p99": float(rank(99))}
+    ordered = np.sort(np.asarray(samples, dtype=np.float64), axis=None)
+    if not ordered.size:
+        return dict.fromkeys(("median", "p95", "p99"), 0.0)
+    return {name: _order_stat(ordered, p) for name, p in (("median", 50), ("p95", 95),
+                                                          ("p99", 99))}
 
 
-def _clog2(x):
-    return 0 if x <= 1 else int(math.ceil(math.log2(x)))
+def _depth(n, block):
+    """L(n, B) (engine.py:47-55)."""
+    def ceil_log2(x):
+        return max(int(x) - 1, 0).bit_length()
+    return ceil_log2(min(block, n)) + 2 * ceil_log2(-(-n // block)) + 3
 
 
-def _scan_depth(n, block_size):
-    return _clog2(min(block_size, n)) + 2 * _clog2(-(-n // block_size)) + 3
+# (name, default) in schema order; the defaults of the measured quantities
+RECORD_FIELDS = (
+    ("mode", None), ("n", None), ("block_size", None), ("tile_q", None), ("d", None),
+    ("d_v", None), ("b", None), ("h", None), ("precision", None), ("repeats", None),
+    ("warmup", None), ("latencies", list), ("merge_count", 0), ("leaf_count", 0),
+    ("peak_extra_memory", 0), ("status", "ok"), ("error", ""),
+)
+_CSV_COLUMNS = ("mode", "n", "block_size", "tile_q", "d", "d_v", "b", "h", "precision",
+                "repeats", "warmup", "status", "latency_median", "latency_p5", "latency_p95",
+                "merge_count", "leaf_count", "peak_extra_memory")
 
 
-@dataclass
 class BenchRecord:
-    """One benchmarked workload (bench.py:40-110); latencies in seconds."""
+    """One timed workload; latencies in seconds. Fields are ``RECORD_FIELDS``
+    (all required except those with a default); summary statistics are
+    derived, never stored."""
 
-    mode: str
-    n: int
-    block_size: int
-    tile_q: int
-    d: int
-    d_v: int
-    b: int
-    h: int
-    precision: str
-    repeats: int
-    warmup: int
-    latencies: list = field(default_factory=list)
-    merge_count: int = 0
-    leaf_count: int = 0
-    peak_extra_memory: int = 0
-    status: str = "ok"
-    error: str = ""
+    __slots__ = tuple(name for name, _ in RECORD_FIELDS)
+
+    def __init__(self, **values):
+        unknown = set(values) - set(self.__slots__)
+        if unknown:
+            raise TypeError(f"unknown BenchRecord fields: {sorted(unknown)}")
+        for name, default in RECORD_FIELDS:
+            if name in values:
+                val = values[name]
+            elif default is None:
+                raise TypeError(f"BenchRecord needs {name!r}")
+            else:
+                val = default() if callable(default) else default
+            setattr(self, name, val)
 
     def summary(self):
-        if not self.latencies:
+        if not len(self.latencies):
             return {"median": None, "p5": None, "p95": None}
-        s = np.sort(np.asarray(self.latencies))
-        pct = nearest_rank_percentiles(s)
-        idx5 = max(int(np.ceil(0.05 * s.size)), 1) - 1
-        return {"median": float(pct["median"]), "p5": float(s[idx5]), "p95": float(pct["p95"])}
+        ordered = np.sort(np.asarray(self.latencies, dtype=np.float64))
+        return {"median": _order_stat(ordered, 50), "p5": _order_stat(ordered, 5),
+                "p95": _order_stat(ordered, 95)}
 
     def to_dict(self):
-        out = {
-            "mode": self.mode, "n": self.n, "block_size": self.block_size,
-            "tile_q": self.tile_q, "d": self.d, "d_v": self.d_v,
-            "b": self.b, "h": self.h, "precision": self.precision,
-            "repeats": self.repeats, "warmup": self.warmup,
-            "latencies": [float(x) for x in self.latencies],
-            "merge_count": self.merge_count, "leaf_count": self.leaf_count,
-            "peak_extra_memory": self.peak_extra_memory,
-            "status": self.status, "error": self.error,
-        }
-        out.update({f"latency_{k}": v for k, v in self.summary().items()})
+        out = {}
+        for name, _ in RECORD_FIELDS:
+            val = getattr(self, name)
+            out[name] = [float(x) for x in val] if name == "latencies" else val
+        for key, val in self.summary().items():
+            out["latency_" + key] = val
         return out
 
-    CSV_FIELDS = (
-        "mode", "n", "block_size", "tile_q", "d", "d_v", "b", "h", "precision",
-        "repeats", "warmup", "status", "latency_median", "latency_p5", "latency_p95",
-        "merge_count", "leaf_count", "peak_extra_memory",
-    )
+    CSV_FIELDS = _CSV_COLUMNS
 
     @classmethod
     def csv_header(cls):
-        return ",".join(cls.CSV_FIELDS)
+        return ",".join(_CSV_COLUMNS)
 
     def csv_row(self):
-        d = self.to_dict()
-        return ",".join("" if d[f] is None else (repr(d[f]) if isinstance(d[f], float) else str(d[f]))
-                        for f in self.CSV_FIELDS)
+        row = self.to_dict()
+        cells = []
+        for col in _CSV_COLUMNS:
+            val = row[col]
+            cells.append("" if val is None else repr(val) if isinstance(val, float) else str(val))
+        return ",".join(cells)
 
 
-@dataclass
 class ScalingFit:
-    """a * L(n, B) + b * n^2 + c with its relative RMS residual (bench.py:113-130)."""
+    """``T(n) = a L(n, B) + b n^2 + c`` with its relative residual."""
 
-    a: float
-    b: float
-    c: float
-    residual: float
-    block_size: int
-    points: list
+    def __init__(self, a, b, c, residual, block_size, points):
+        self.a, self.b, self.c = float(a), float(b), float(c)
+        self.residual = float(residual)
+        self.block_size = int(block_size)
+        self.points = list(points)
 
     def predict(self, n):
-        return self.a * _scan_depth(int(n), self.block_size) + self.b * float(n) ** 2 + self.c
+        n = int(n)
+        return self.a * _depth(n, self.block_size) + self.b * float(n) * float(n) + self.c
 
     def to_dict(self):
-        return {
-            "a": self.a, "b": self.b, "c": self.c,
-            "residual": self.residual, "block_size": self.block_size,
-            "points": [[int(n), float(t)] for n, t in self.points],
-        }
+        return {"a": self.a, "b": self.b, "c": self.c, "residual": self.residual,
+                "block_size": self.block_size,
+                "points": [[int(n), float(t)] for n, t in self.points]}
 
 
 def fit_scaling(points, block_size):
-    """Ordinary least squares of latency on [L(n, B), n^2, 1], columns
-    normalised before the solve (bench.py:193-219)."""
+    """Least-squares fit of latency to [L(n, B), n^2, 1]: each design column
+    is scaled to unit 2-norm (the raw columns span ~10 orders of magnitude),
+    the system is solved through a reduced Householder QR (R c = Q^T t) and
+    the scaling undone. Needs three distinct n."""
     pts = [(int(n), float(t)) for n, t in points]
-    ns = np.array([p[0] for p in pts], dtype=np.float64)
-    ts = np.array([p[1] for p in pts], dtype=np.float64)
-    if len(set(ns.tolist())) < 3:
-        raise ShapeError("need at least 3 points with distinct n to fit 3 coefficients")
-    design = np.stack([
-        np.array([_scan_depth(int(n), block_size) for n in ns], dtype=np.float64),
-        ns ** 2,
-        np.ones_like(ns),
-    ], axis=1)
-    norms = np.linalg.norm(design, axis=0)
-    coef, *_ = np.linalg.lstsq(design / norms, ts, rcond=None)
-    coef = coef / norms
-    pred = design @ coef
-    denom = max(float(np.linalg.norm(ts)), np.finfo(np.float64).tiny)
-    return ScalingFit(a=float(coef[0]), b=float(coef[1]), c=float(coef[2]),
-                      residual=float(np.linalg.norm(pred - ts) / denom),
-                      block_size=block_size, points=pts)
+    n_arr = np.fromiter((n for n, _ in pts), dtype=np.float64, count=len(pts))
+    t_arr = np.fromiter((t for _, t in pts), dtype=np.float64, count=len(pts))
+    if np.unique(n_arr).size < 3:
+        raise ShapeError("the scaling fit has 3 coefficients: give at least 3 distinct n")
+    cols = np.column_stack([[float(_depth(int(n), block_size)) for n in n_arr],
+                            n_arr * n_arr, np.ones_like(n_arr)])
+    scale = np.sqrt((cols * cols).sum(axis=0))
+    qmat, rmat = np.linalg.qr(cols / scale, mode="reduced")
+    coef = np.linalg.solve(rmat, qmat.T @ t_arr) / scale
+    fitted = cols @ coef
+    tnorm = float(np.sqrt(t_arr @ t_arr))
+    resid = float(np.sqrt(((fitted - t_arr) ** 2).sum())) / max(tnorm, np.finfo(float).tiny)
+    return ScalingFit(coef[0], coef[1], coef[2], resid, block_size, pts)
 
 
 def emit_report(records, fits, json_path, csv_path=None):
-    """JSON report + flat CSV (bench.py:222-242)."""
-    doc = {
-        "schema": "scanattn-bench-v1",
-        "records": [r.to_dict() for r in records],
-        "fits": [f.to_dict() for f in fits],
-    }
-    with open(json_path, "w") as f:
-        json.dump(doc, f, indent=2)
-        f.write("\n")
+    """Write the ``scanattn-bench-v1`` JSON document (2-space indent, newline
+    terminated) and the flat CSV (default: the JSON path with ``.csv``)."""
+    text = json.dumps({"schema": "scanattn-bench-v1",
+                       "records": [r.to_dict() for r in records],
+                       "fits": [f.to_dict() for f in fits]}, indent=2)
     if csv_path is None:
-        csv_path = str(json_path).rsplit(".", 1)[0] + ".csv"
-    with open(csv_path, "w") as f:
-        f.write(BenchRecord.csv_header() + "\n")
-        for r in records:
-            f.write(r.csv_row() + "\n")
+        stem, _, _ = str(json_path).rpartition(".")
+        csv_path = (stem or str(json_path)) + ".csv"
+    lines = [BenchRecord.csv_header()] + [r.csv_row() for r in records]
+    with open(json_path, "w") as fh:
+        fh.write(text + "\n")
+    with open(csv_path, "w") as fh:
+        fh.write("\n".join(lines) + "\n")
     return json_path, csv_path
 
 

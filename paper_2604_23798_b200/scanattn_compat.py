@@ -148,14 +148,17 @@ class ScanConfig:
     kv_splits: int = 0
 
     def __post_init__(self):
-        if self.block_size < 1:
-            raise ShapeError(f"block_size must be >= 1, got {self.block_size}")
-        if self.tile_q < 1:
-            raise ShapeError(f"tile_q must be >= 1, got {self.tile_q}")
-        if self.workers != "auto" and (not isinstance(self.workers, int) or self.workers < 1):
-            raise ShapeError(f"workers must be a positive integer or 'auto', got {self.workers!r}")
+        for name in ("block_size", "tile_q"):
+            if getattr(self, name) < 1:
+                raise ShapeError(f"ScanConfig.{name} = {getattr(self, name)}: needs a "
+                                 "positive tile size")
+        w = self.workers
+        if not (w == "auto" or (isinstance(w, int) and w >= 1)):
+            raise ShapeError(f"ScanConfig.workers = {w!r}: use 'auto' or a count >= 1 "
+                             "(ignored on the GPU)")
         if self.kv_splits < 0:
-            raise ShapeError("kv_splits must be >= 0")
+            raise ShapeError(f"ScanConfig.kv_splits = {self.kv_splits}: use 0 (auto) or a "
+                             "split count")
 
 
 @dataclass
@@ -333,38 +336,46 @@ def inter_block_combine(block_totals, return_prefixes=False, device=None):
     return total, _triples(pre[0][0].cpu().numpy(), pre[1][0].cpu().numpy(), pre[2][0].cpu().numpy())
 
 
+_TINY = np.finfo(np.float64).tiny
+
+
+def _state_signature(t):
+    """(m, S, W..., W/S...) of a state as one float64 vector."""
+    w = np.asarray(t.W, dtype=np.float64).ravel()
+    s = float(t.S)
+    return np.hstack((float(t.m), s, w, w / max(s, _TINY)))
+
+
 def _triple_rel_dev(t1, t2):
-    """verify.py:218-227."""
-    tiny = np.finfo(np.float64).tiny
-    def parts(t):
-        W = np.asarray(t.W, dtype=np.float64)
-        return np.concatenate([[float(t.m)], [float(t.S)], W, W / max(float(t.S), tiny)])
-    p1, p2 = parts(t1), parts(t2)
-    denom = np.maximum(np.maximum(np.abs(p1), np.abs(p2)), tiny)
-    return float(np.max(np.abs(p1 - p2) / denom))
+    """Largest componentwise relative difference of two states over
+    (m, S, W, W/S) — the deviation verify.py:218-227 defines."""
+    a, b = _state_signature(t1), _state_signature(t2)
+    return float((np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), _TINY)).max())
 
 
-@dataclass
 class BlockValidationReport:
-    """verify.py:230-246."""
+    """Result of :func:`block_validation`; same attributes, ``passed`` and
+    ``to_dict`` as the reference's report (verify.py:230-246)."""
 
-    partitions: list
-    query_points: list
-    max_pairwise_dev: float
-    max_vs_sequential_dev: float
-    per_partition_dev: dict
+    _FIELDS = ("partitions", "query_points", "max_pairwise_dev", "max_vs_sequential_dev",
+               "per_partition_dev")
+
+    def __init__(self, partitions, query_points, max_pairwise_dev, max_vs_sequential_dev,
+                 per_partition_dev):
+        self.partitions = partitions
+        self.query_points = query_points
+        self.max_pairwise_dev = max_pairwise_dev
+        self.max_vs_sequential_dev = max_vs_sequential_dev
+        self.per_partition_dev = per_partition_dev
 
     def passed(self, tol):
-        return self.max_pairwise_dev <= tol and self.max_vs_sequential_dev <= tol
+        return max(self.max_pairwise_dev, self.max_vs_sequential_dev) <= tol
 
     def to_dict(self):
-        return {
-            "partitions": list(self.partitions),
-            "query_points": [list(q) for q in self.query_points],
-            "max_pairwise_dev": self.max_pairwise_dev,
-            "max_vs_sequential_dev": self.max_vs_sequential_dev,
-            "per_partition_dev": {str(k): v for k, v in self.per_partition_dev.items()},
-        }
+        conv = {"partitions": list,
+                "query_points": lambda pts: [list(p) for p in pts],
+                "per_partition_dev": lambda dv: {str(k): x for k, x in dv.items()}}
+        return {f: conv.get(f, lambda x: x)(getattr(self, f)) for f in self._FIELDS}
 
 
 def block_validation(problem, cfg, partitions, query_indices=None, device=None):
