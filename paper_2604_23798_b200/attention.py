@@ -163,9 +163,9 @@ def describe_plan(q, k, v, kv_splits=0):
     """The launch plan (kernel configuration, tiles, kv splits) for these shapes."""
     q4, k4, v4 = _as_4d(q, "query"), _as_4d(k, "key"), _as_4d(v, "value")
     shp = _shape(q4, k4, v4)
-    buf = ctypes.create_string_buffer(128)
+    buf = ctypes.create_string_buffer(256)
     with torch.cuda.device(_plan_device(q4)):
-        _lib.check_status(_lib.lib().elsa_describe_plan(ctypes.byref(shp), int(kv_splits), buf, 128),
+        _lib.check_status(_lib.lib().elsa_describe_plan(ctypes.byref(shp), int(kv_splits), buf, 256),
                           "elsa_describe_plan")
     return buf.value.decode()
 
@@ -190,6 +190,10 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
         raise ShapeError("is_causal is not supported: the reference computes full "
                          "(bidirectional) attention only")
     _validate(query, key, value, allow_16bit=True)
+    if torch.is_grad_enabled() and any(t.requires_grad for t in (query, key, value)):
+        raise ShapeError("the ELSA path is forward-only (the reference has no backward): "
+                         "call it under torch.no_grad() or on tensors without requires_grad "
+                         "instead of silently cutting the gradient")
     orig_dim = query.dim()
     orig_shape = query.shape
     q, k, v = (_prep(_as_4d(t, n)) for t, n in ((query, "query"), (key, "key"), (value, "value")))
@@ -212,8 +216,9 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
         y = torch.empty((B, H, n_q, dv), device=q.device, dtype=torch.float32)
     else:
         y = out
+        overlapping = any(s_ <= 0 for s_, n_ in zip(y.stride()[:3], y.shape[:3]) if n_ > 1)
         if tuple(y.shape) != (B, H, n_q, dv) or y.dtype != torch.float32 or y.device != q.device \
-                or y.stride(-1) != 1:
+                or y.stride(-1) != 1 or overlapping:
             raise ShapeError("out must be a float32 (B, H, n_q, dv) tensor on the input device "
                              "with a contiguous last axis")
     # shape struct + workspace size per geometry (cheap repeat calls)
@@ -336,8 +341,12 @@ def _sdpa_tc(q, k, v, sc, out):
         # TMA operands: 16-byte aligned base and row strides. Otherwise copy
         # into a buffer whose rows are padded to a multiple of 8 elements
         # (the kernel reads the first d columns; TMA zero-fills the box).
+        # A zero stride (an expanded / broadcast axis, e.g. K/V shared across
+        # heads) passes the modulo test but is no valid TMA stride:
+        # materialise such inputs into the padded copy too.
         if t.stride(-1) == 1 and t.data_ptr() % 16 == 0 and all(
-                (s * 2) % 16 == 0 for s in t.stride()[:3]):
+                s > 0 and (s * 2) % 16 == 0 for s, n in zip(t.stride()[:3], t.shape[:3])
+                if n > 1):
             return t
         w = t.shape[-1]
         buf = torch.empty((*t.shape[:-1], -(-w // 8) * 8), device=t.device, dtype=t.dtype)
@@ -345,12 +354,18 @@ def _sdpa_tc(q, k, v, sc, out):
         return buf[..., :w]
 
     q, k, v = (tma_ready(t) for t in (q, k, v))
+    dest = None
     if out is None:
         y = torch.empty((B, H, n_q, dv), device=q.device, dtype=q.dtype)
     else:
         y = out
         if tuple(y.shape) != (B, H, n_q, dv) or y.dtype != q.dtype or y.device != q.device:
             raise ShapeError("out must match the query's dtype/device with shape (B, H, n_q, dv)")
+        if y.stride(-1) != 1 or any(s <= 0 for s, n in zip(y.stride()[:3], y.shape[:3])
+                                    if n > 1):
+            # K5 stores each Y row as contiguous columns: write a dense
+            # temporary and copy it into the caller's strided view
+            dest, y = y, torch.empty((B, H, n_q, dv), device=q.device, dtype=q.dtype)
     shp = _shape(q, k, v, y)
     with torch.cuda.device(q.device):
         st = _lib.lib().elsa_fwd_f16(
@@ -358,6 +373,9 @@ def _sdpa_tc(q, k, v, sc, out):
             ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(y.data_ptr()), ctypes.byref(shp),
             ctypes.c_double(sc), 1 if q.dtype == torch.bfloat16 else 0, _stream_ptr(q.device))
         _lib.check_status(st, "elsa_fwd_f16")
+    if dest is not None:
+        dest.copy_(y)
+        return dest
     return y
 
 

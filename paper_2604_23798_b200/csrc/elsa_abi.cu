@@ -315,11 +315,15 @@ Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms) {
       lo = hi = normalize_splits(requested, tiles);
     } else {
       hi = tiles < kMaxSplits ? tiles : kMaxSplits;
-      // splits of even a single head must fit the workspace budget
-      const int64_t ws_cap = head_bytes > 0 ? workspace_budget() / head_bytes : hi;
-      if (hi > ws_cap) hi = ws_cap < 1 ? 1 : ws_cap;
+      // the chain cap wins over the workspace budget: the fewest splits that
+      // keep every CTA's chain <= kMaxChainTiles are always allowed (the
+      // workspace then exceeds the soft budget for a single head); beyond
+      // kMaxSplits * kMaxChainTiles tiles the chain grows and describe_plan
+      // reports it
       lo = ceil_div(tiles, kMaxChainTiles);
       if (lo > hi) lo = hi;
+      const int64_t ws_cap = head_bytes > 0 ? workspace_budget() / head_bytes : hi;
+      if (hi > ws_cap) hi = ws_cap < lo ? lo : ws_cap;
     }
     for (int64_t s = lo; s <= hi; ++s) {
       const int64_t sn = normalize_splits(s, tiles);
@@ -1307,9 +1311,14 @@ int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n
   if (pl.cfg < 0 || pl.cfg > kCfgW4R8D256V256) return ELSA_ERR_SHAPE;
   const CfgInfo ci = cfg_info(pl.cfg);
   const int64_t slices = ceil_div(shp->dv, cfg_dv(pl.cfg));
+  const int64_t chain = ceil_div(ceil_div(shp->n_kv, ci.tk), pl.splits);
+  std::string extra = slices > 1 ? " dv_slices=" + std::to_string(slices) : std::string();
+  if (chain > kMaxChainTiles)
+    extra += " chain_tiles=" + std::to_string(chain) + " (over the " +
+             std::to_string(kMaxChainTiles) + "-tile cap: > kMaxSplits x cap keys)";
   std::snprintf(buf, n, "%s tq=%d tk=%d kv_splits=%d heads_per_batch=%lld%s", names[pl.cfg],
                 ci.tq, ci.tk, pl.splits, static_cast<long long>(pl.heads_per_batch),
-                slices > 1 ? (" dv_slices=" + std::to_string(slices)).c_str() : "");
+                extra.c_str());
   return ELSA_OK;
 }
 

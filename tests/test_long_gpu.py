@@ -105,3 +105,16 @@ def test_c5_kv_sharded_peer_and_nccl(c5, pg):
     elsa.check_device_error(DEV)
     assert torch.equal(y_peer, y_nccl)
     _check(y_peer, sel, ref, "C5 kv-sharded (8 chunks)")
+
+
+def test_chain_cap_holds_when_workspace_budget_binds():
+    """A 2^20-row head at 2^20 keys: the 4 GiB split-workspace budget alone
+    would allow 15 splits (a 1093-tile chain); the planner keeps the chain
+    cap (>= 16 splits) and the workspace grows past the soft budget. Beyond
+    kMaxSplits x 1024 tiles the over-long chain is reported by describe_plan."""
+    q = torch.empty(1, 1, N_KV, 64, device=DEV)
+    plan = elsa.describe_plan(q, q, q)
+    assert elsa.resolve_kv_splits(q, q, q) >= 16 and "chain_tiles" not in plan, plan
+    kk = torch.empty(1, 1, 1 << 22, 64, device=DEV)   # 65536 tiles > 32 x 1024
+    plan = elsa.describe_plan(q[:, :, :1024], kk, kk)
+    assert "chain_tiles=2048" in plan, plan

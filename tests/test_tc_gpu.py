@@ -157,3 +157,31 @@ def test_tc_d128_aliased_p_stress_deterministic():
     ref = elsa.scaled_dot_product_attention(qb.float(), kb.float(), vb.float())
     err = ((y1.float() - ref).norm(dim=-1) / ref.norm(dim=-1)).max().item()
     assert err < 2e-2, err
+
+
+def test_tc_strided_out_and_expanded_kv():
+    """A transposed `out` gets the values in the right elements (K5 writes a
+    dense temporary, then copies); K/V expanded over heads (stride 0) are
+    materialised instead of rejected."""
+    g = torch.Generator(device=DEV)
+    g.manual_seed(77)
+    q = torch.randn(1, 4, 256, 64, device=DEV, generator=g).to(torch.bfloat16)
+    k1 = torch.randn(1, 1, 300, 64, device=DEV, generator=g).to(torch.bfloat16)
+    v1 = torch.randn(1, 1, 300, 64, device=DEV, generator=g).to(torch.bfloat16)
+    k, v = k1.expand(1, 4, 300, 64), v1.expand(1, 4, 300, 64)
+    assert k.stride(1) == 0
+    ref = elsa.scaled_dot_product_attention(q, k.contiguous(), v.contiguous())
+    y = elsa.scaled_dot_product_attention(q, k, v)
+    assert torch.equal(y, ref)
+    base = torch.empty(1, 4, 64, 256, device=DEV, dtype=torch.bfloat16)
+    out = base.transpose(-1, -2)          # last-axis stride 256
+    r = elsa.scaled_dot_product_attention(q, k, v, out=out)
+    assert r.data_ptr() == out.data_ptr() and torch.equal(out, ref)
+
+
+def test_requires_grad_is_rejected_loudly():
+    q = torch.randn(1, 1, 64, 64, device=DEV, requires_grad=True)
+    with pytest.raises(elsa.ShapeError):
+        elsa.scaled_dot_product_attention(q, q.detach(), q.detach())
+    with torch.no_grad():
+        elsa.scaled_dot_product_attention(q, q, q)
