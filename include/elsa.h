@@ -79,8 +79,15 @@ int elsa_scan_depth(int64_t n, int64_t block_size);
 int elsa_resolve_kv_splits(const elsa_shape* shp, int requested);
 
 /* Workspace bytes elsa_fwd_f32 needs for `kv_splits` (0 = auto). Zero when
- * the resolved split count is 1. */
+ * the resolved split count is 1 or the splits merge inside the launch
+ * (thread-block-cluster merge over distributed shared memory). */
 size_t elsa_workspace_bytes(const elsa_shape* shp, int kv_splits);
+
+/* Workspace bytes elsa_partial_f32 needs for keys [kv_begin, kv_end) and
+ * `kv_splits` (0 = auto): partial states always merge through the split
+ * workspace (their output is a state, not Y). */
+size_t elsa_partial_workspace_bytes(const elsa_shape* shp, int64_t kv_begin, int64_t kv_end,
+                                    int kv_splits);
 
 /* Y = softmax(Q K^T * scale) V, FP32 in, FP32 FFMA arithmetic, FP32 out.
  * kv_splits: 0 = auto, else the number of contiguous key-range partitions

@@ -26,6 +26,7 @@ EXPORTED_SYMBOLS = (
     "elsa_scan_depth",
     "elsa_resolve_kv_splits",
     "elsa_workspace_bytes",
+    "elsa_partial_workspace_bytes",
     "elsa_fwd_f32",
     "elsa_host_workspace_bytes",
     "elsa_fwd_f32_host",
@@ -90,6 +91,12 @@ def _declare(h):
     h.elsa_resolve_kv_splits.argtypes = [shp, c_int]
     h.elsa_workspace_bytes.restype = c_sz
     h.elsa_workspace_bytes.argtypes = [shp, c_int]
+    h.elsa_partial_workspace_bytes.restype = c_sz
+    h.elsa_partial_workspace_bytes.argtypes = [shp, c_i64, c_i64, c_int]
+    # development aid (not in include/elsa.h): cluster-merge mode 0 / 1 / 2
+    if hasattr(h, "elsa_dev_set_cluster"):
+        h.elsa_dev_set_cluster.restype = None
+        h.elsa_dev_set_cluster.argtypes = [c_int]
     h.elsa_fwd_f32.restype = c_int
     h.elsa_fwd_f32.argtypes = [c_vp, c_vp, c_vp, c_vp, shp, c_dbl, c_int, c_vp, c_sz, c_vp]
     h.elsa_host_workspace_bytes.restype = c_sz

@@ -46,7 +46,8 @@ MAX_D = 256
 MAX_DV = 4096
 
 def _stream_ptr(device):
-    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(idx))
 
 
 def _as_4d(t, name):
@@ -181,6 +182,11 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
     synchronises and raises :class:`NumericalError` on a bad normalizer, the
     way the reference raises from ``scan_forward`` (engine.py:377-378).
     """
+    if (attn_mask is None and not dropout_p and not is_causal and out is None
+            and not check_numerics):
+        y = _fast_f32(query, key, value, scale, kv_splits)
+        if y is not None:
+            return y
     if attn_mask is not None:
         raise ShapeError("attn_mask is not supported: masks are a non-goal of the ELSA "
                          "FP32 path (SPEC.md:242)")
@@ -234,7 +240,8 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
                 _SHAPE_CACHE.clear()
             _SHAPE_CACHE[key] = hit
         shp, ws_bytes = hit
-        ws = torch.empty(max(ws_bytes, 1), device=q.device, dtype=torch.uint8) if ws_bytes else None
+        ws = (_split_workspace(q.device.index, torch._C._cuda_getCurrentRawStream(q.device.index),
+                               ws_bytes) if ws_bytes else None)
         st = h.elsa_fwd_f32(
             ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),
             ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(y.data_ptr()), ctypes.byref(shp),
@@ -247,6 +254,83 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
     if orig_dim == 4 or out is not None:
         return y
     return y.reshape(*orig_shape[:-1], dv)
+
+
+_FAST = {}   # (shapes, strides, kv_splits, device) -> (ElsaShape, ws bytes, scale, Y shape)
+_SPLIT_WS = {}  # (device, stream) -> split workspace reused by calls on that stream
+
+
+def _split_workspace(dev_idx, stream, nbytes):
+    """Split workspace for elsa_fwd_f32, kept per (device, stream) and grown
+    on demand: calls on one stream are ordered, so reuse is safe."""
+    key = (dev_idx, stream)
+    ws = _SPLIT_WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        if len(_SPLIT_WS) > 64:
+            _SPLIT_WS.clear()
+        ws = torch.empty(nbytes, device=torch.device("cuda", dev_idx), dtype=torch.uint8)
+        _SPLIT_WS[key] = ws
+    return ws
+
+
+def _fast_f32(q, k, v, scale, kv_splits):
+    """The common case without Python-side reshaping: 4-D float32 CUDA
+    tensors on one device with contiguous last axes, no `out`, no gradient.
+    Returns None to fall back to the general path (which validates and
+    raises). Per-geometry state (the shape struct, workspace size, scale) is
+    cached; the split workspace is reused per stream."""
+    f32 = torch.float32
+    if not (type(q) is torch.Tensor and type(k) is torch.Tensor and type(v) is torch.Tensor):
+        return None
+    if q.dtype is not f32 or k.dtype is not f32 or v.dtype is not f32:
+        return None
+    if q.dim() != 4 or k.dim() != 4 or v.dim() != 4:
+        return None
+    if q.requires_grad or k.requires_grad or v.requires_grad:
+        return None
+    dev_idx = q.get_device()
+    if dev_idx < 0 or k.get_device() != dev_idx or v.get_device() != dev_idx:
+        return None
+    qs, ks, vs = q.stride(), k.stride(), v.stride()
+    if qs[3] != 1 or ks[3] != 1 or vs[3] != 1:
+        return None
+    key_ = (q.shape, qs, k.shape, ks, v.shape, vs, kv_splits, dev_idx, scale)
+    hit = _FAST.get(key_)
+    if hit is None:
+        if any(x.shape[-1] == 0 for x in (q, k, v)):
+            return None
+        B, H, n_q, d = q.shape
+        sc = (1.0 / math.sqrt(d)) if scale is None else float(scale)
+        if not math.isfinite(sc):
+            return None
+        yshape = (B, H, n_q, v.shape[-1])
+        shp = _shape(q, k, v)   # raises ShapeError on bad geometry
+        dv = yshape[3]
+        shp.y_stride[0], shp.y_stride[1], shp.y_stride[2] = H * n_q * dv, n_q * dv, dv
+        with torch.cuda.device(q.device):
+            ws_bytes = _lib.lib().elsa_workspace_bytes(ctypes.byref(shp), int(kv_splits))
+        if len(_FAST) > 256:
+            _FAST.clear()
+        hit = (shp, ws_bytes, ctypes.c_double(sc), yshape)
+        _FAST[key_] = hit
+    shp, ws_bytes, sc, yshape = hit
+    y = torch.empty(yshape, device=q.device, dtype=f32)
+    stream = torch._C._cuda_getCurrentRawStream(dev_idx)
+    ws_ptr = _split_workspace(dev_idx, stream, ws_bytes).data_ptr() if ws_bytes else 0
+    h = _lib.lib()
+    cur = torch._C._cuda_getDevice()
+    if cur != dev_idx:
+        torch._C._cuda_setDevice(dev_idx)
+    try:
+        st = h.elsa_fwd_f32(q.data_ptr(), k.data_ptr(), v.data_ptr(), y.data_ptr(),
+                            ctypes.byref(shp), sc, int(kv_splits), ws_ptr, ws_bytes,
+                            stream)
+    finally:
+        if cur != dev_idx:
+            torch._C._cuda_setDevice(cur)
+    if st:
+        _lib.check_status(st, "elsa_fwd_f32")
+    return y
 
 
 _HOST_WS = {}
@@ -414,9 +498,8 @@ def partial_states(query, key, value, kv_begin=0, kv_end=None, scale=None, kv_sp
         ws_bytes = 0
         if kv_splits != 1:
             # the plan (and its workspace) is made for the key range, not n_kv
-            rng = _lib.ElsaShape.from_buffer_copy(shp)
-            rng.n_kv = max(int(kv_end) - int(kv_begin), 1)
-            ws_bytes = h.elsa_workspace_bytes(ctypes.byref(rng), int(kv_splits))
+            ws_bytes = h.elsa_partial_workspace_bytes(ctypes.byref(shp), int(kv_begin),
+                                                      int(kv_end), int(kv_splits))
         ws = torch.empty(max(ws_bytes, 1), device=q.device, dtype=torch.uint8) if ws_bytes else None
         st = h.elsa_partial_f32(
             ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),
@@ -550,6 +633,19 @@ def inter_block_combine(m, S, W, return_prefixes=False):
             ptr(ws), ctypes.c_size_t(ws_bytes), _stream_ptr(dev))
         _lib.check_status(st, "elsa_block_scan_f32")
     return ((tm, tS, tW), pre) if return_prefixes else (tm, tS, tW)
+
+
+def set_cluster_mode(mode):
+    """Development aid: 0 = never merge kv splits inside the launch (always
+    K1 + K2), 1 = when the planner's cost model prefers it (default), 2 =
+    whenever the configuration allows it. Clears the per-geometry workspace
+    cache, whose sizes depend on the mode."""
+    h = _lib.lib()
+    if not hasattr(h, "elsa_dev_set_cluster"):
+        raise ShapeError("this libelsa build has no cluster-merge control")
+    h.elsa_dev_set_cluster(int(mode))
+    _SHAPE_CACHE.clear()
+    _FAST.clear()
 
 
 def ffma_peak_tflops(device=None):

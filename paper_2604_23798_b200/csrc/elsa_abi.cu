@@ -69,11 +69,17 @@ int cuda_fail(cudaError_t e, const char* where) {
   return ELSA_ERR_CUDA;
 }
 
+constexpr int kCluAttrBase = kAttrSlots;  // attribute slots of the cluster-merge kernels
 struct DeviceCache {
   bool ready = false;
   int sms = 0;
   int* err = nullptr;
-  bool attr[kAttrSlots] = {};  // forward configs x TMA flag, then the tc kernels
+  bool attr[2 * kAttrSlots] = {};  // forward configs x TMA flag, then the tc kernels; cluster kernels
+  int clusters[2][17];             // max active clusters: [w4r8, w8r8][splits], -1 = unknown
+  DeviceCache() {
+    for (auto& row : clusters)
+      for (int& x : row) x = -1;
+  }
 };
 DeviceCache g_dev[kMaxDevices];
 std::mutex g_mu;
@@ -273,7 +279,15 @@ struct Plan {
   int cfg;
   int splits;
   int64_t heads_per_batch;  // (b, h) pairs per launch batch when splits > 1
+  bool cluster = false;     // splits merged inside one launch over DSMEM (no workspace, no K2)
 };
+
+// Cluster split merge (fwd_f32_kernel<..., CL = true>): the d, dv <= 64
+// configurations with 2..16 splits, final output only.
+constexpr int kMaxClusterSplits = 16;
+bool cluster_capable(int cfg, int64_t dv) {
+  return (cfg == kCfgW4R8 || cfg == kCfgW8R8) && dv <= 64;
+}
 
 double plan_cost(const CfgInfo& ci, int64_t ctas, int64_t tiles, int64_t rows, int64_t sms,
                  int64_t s) {
@@ -292,7 +306,28 @@ int64_t normalize_splits(int64_t s, int64_t tiles) {
   return ceil_div(tiles, tps);
 }
 
-Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms) {
+// Cluster-merge mode (development aid, elsa_dev_set_cluster): 0 never,
+// 1 when the cost model prefers it (default), 2 whenever capable.
+int g_cluster_mode = [] {
+  const char* e = std::getenv("ELSA_CLUSTER");
+  return e ? std::atoi(e) : 1;
+}();
+constexpr int kClusterAutoMaxSplits = 4;
+
+template <int W, int TK, int ST, int R>
+int max_active_clusters(int splits, DeviceCache* dc, int cfg_slot);
+
+int cluster_slot(int cfg) { return cfg == kCfgW8R8 ? 1 : 0; }
+
+int active_clusters(int cfg, int splits, DeviceCache* dc) {
+  if (!dc || splits < 2 || splits > kMaxClusterSplits) return 0;
+  return cfg == kCfgW8R8
+             ? max_active_clusters<8, 64, ELSA_W8R8_STAGES, 8>(splits, dc, cluster_slot(cfg))
+             : max_active_clusters<4, 64, ELSA_W4R8_STAGES, 8>(splits, dc, cluster_slot(cfg));
+}
+
+Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms,
+              bool allow_cluster = false, DeviceCache* dc = nullptr) {
   const int64_t BH = sh->B * sh->H;
   // head widths beyond 64 have one configuration each; d, dv <= 64 choose
   const int only = wide_cfg(sh->d, sh->dv);
@@ -341,6 +376,25 @@ Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms) {
       }
     }
   }
+  // Cluster split merge (fwd_f32_kernel<..., CL>): the chosen plan's splits
+  // merge inside the launch over DSMEM instead of through the workspace and
+  // K2. Measured on B200 (tools/time_cluster.py, profiles/round2_cluster.md),
+  // it pays only while every cluster is resident at once and clusters are
+  // small: 8- and 16-CTA clusters of the 2-CTA/SM w4r8 kernel get packed two
+  // CTAs per SM (C1: 19.7 us vs 12.9 + 4.5 us for K1 + K2), and multi-wave
+  // cluster launches lose to the free placement of a plain grid (B1 H1 n16K,
+  // 4 splits: 1421 vs 1256 us). So the auto plan converts a 2..4-split plan
+  // whose clusters all fit at once; mode 2 converts whatever can launch.
+  if (allow_cluster && g_cluster_mode != 0 && best.splits > 1 &&
+      best.splits <= kMaxClusterSplits && cluster_capable(best.cfg, sh->dv)) {
+    const int maxc = active_clusters(best.cfg, best.splits, dc);
+    const int64_t nclu = ceil_div(sh->n_q, cfg_info(best.cfg).tq) * BH;
+    const bool fits = maxc > 0 && nclu <= maxc && best.splits <= kClusterAutoMaxSplits;
+    if (fits || (g_cluster_mode == 2 && maxc > 0)) {
+      best.cluster = true;
+      best.heads_per_batch = BH;
+    }
+  }
   return best;
 }
 
@@ -362,8 +416,53 @@ bool tma_ok(const float* base, const int64_t st[3], int64_t inner) {
   return true;
 }
 
+// Per-thread cache of encoded descriptors: eager callers re-run the same
+// geometry on the same buffers, and encoding three maps per call is a visible
+// share of a small problem's host time. Keyed by everything the map encodes.
+struct MapKey {
+  const void* base;
+  int64_t dims[4], st[3];
+  int box_inner, box_rows;
+  bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof(MapKey)) == 0; }
+};
+struct MapEntry {
+  MapKey key;
+  CUtensorMap map;
+  bool valid = false;
+};
+constexpr int kMapCache = 32;
+thread_local MapEntry t_maps[kMapCache];
+
+bool encode_map_uncached(CUtensorMap* map, const float* base, int64_t inner, int64_t rows,
+                         int64_t H, int64_t B, const int64_t st[3], int box_inner, int box_rows);
+
 bool encode_map(CUtensorMap* map, const float* base, int64_t inner, int64_t rows, int64_t H,
                 int64_t B, const int64_t st[3], int box_inner, int box_rows) {
+  MapKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.base = base;
+  key.dims[0] = inner, key.dims[1] = rows, key.dims[2] = H, key.dims[3] = B;
+  key.st[0] = st[0], key.st[1] = st[1], key.st[2] = st[2];
+  key.box_inner = box_inner, key.box_rows = box_rows;
+  uint64_t hsh = reinterpret_cast<uintptr_t>(base) >> 4;
+  for (int i = 0; i < 4; ++i) hsh = hsh * 1000003u ^ uint64_t(key.dims[i]);
+  for (int i = 0; i < 3; ++i) hsh = hsh * 1000003u ^ uint64_t(key.st[i]);
+  hsh = hsh * 1000003u ^ uint64_t(box_inner * 4096 + box_rows);
+  MapEntry& e = t_maps[(hsh ^ (hsh >> 29)) % kMapCache];
+  if (e.valid && e.key == key) {
+    *map = e.map;
+    return true;
+  }
+  if (!encode_map_uncached(map, base, inner, rows, H, B, st, box_inner, box_rows)) return false;
+  e.key = key;
+  e.map = *map;
+  e.valid = true;
+  return true;
+}
+
+bool encode_map_uncached(CUtensorMap* map, const float* base, int64_t inner, int64_t rows,
+                         int64_t H, int64_t B, const int64_t st[3], int box_inner,
+                         int box_rows) {
   auto enc = encoder();
   if (!enc) return false;
   cuuint64_t dims[4] = {cuuint64_t(inner), cuuint64_t(rows), cuuint64_t(H), cuuint64_t(B)};
@@ -376,7 +475,7 @@ bool encode_map(CUtensorMap* map, const float* base, int64_t inner, int64_t rows
   return r == CUDA_SUCCESS;
 }
 
-template <int W, int TK, int ST, int R, int D = 64, int DV = 64>
+template <int W, int TK, int ST, int R, int D = 64, int DV = 64, bool CL = false>
 int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[3],
                    int64_t v_st[3], int splits, int64_t bh_count, int cfg_slot, DeviceCache* dc,
                    cudaStream_t stream) {
@@ -406,30 +505,98 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
   static const bool force_generic = std::getenv("ELSA_FORCE_GENERIC_LOAD") != nullptr;
   if (force_generic) use_tma = false;
 
-  auto kern = fwd_f32_kernel<W, TK, ST, R, false, D, DV>;
+  auto kern = fwd_f32_kernel<W, TK, ST, R, false, D, DV, CL>;
   if constexpr (T::QP <= 256) {
-    if (use_tma) kern = fwd_f32_kernel<W, TK, ST, R, true, D, DV>;
+    if (use_tma) kern = fwd_f32_kernel<W, TK, ST, R, true, D, DV, CL>;
   }
-  const int slot = cfg_slot * 2 + (use_tma ? 1 : 0);
+  const int slot = (CL ? kCluAttrBase : 0) + cfg_slot * 2 + (use_tma ? 1 : 0);
   if (!dc->attr[slot]) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               int(T::SMEM_BYTES));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(T::SMEM_BYTES));
+    if (e == cudaSuccess && CL)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fwd)");
     dc->attr[slot] = true;
   }
   const int64_t gx = int64_t(p.qtiles) * bh_count;
   if (gx >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
   const dim3 grid{unsigned(gx), unsigned(splits), unsigned(ceil_div(s->dv, DV))};
-  kern<<<grid, T::THREADS, T::SMEM_BYTES, stream>>>(p, maps[0], maps[1], maps[2]);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "fwd launch");
+  if constexpr (CL) {
+    // ELSA_CLUSTER_SOLO=1 (experiment): pad the shared-memory request so a
+    // cluster's CTAs spread one per SM instead of packing two per SM
+    static const bool solo = std::getenv("ELSA_CLUSTER_SOLO") != nullptr;
+    size_t smem = T::SMEM_BYTES;
+    if (solo && smem < 120 * 1024) smem = 120 * 1024;
+    if (solo) {
+      const cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  int(smem));
+      if (e2 != cudaSuccess) return cuda_fail(e2, "cudaFuncSetAttribute(fwd solo)");
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(T::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = unsigned(splits);
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, maps[0], maps[1], maps[2]);
+    if (e != cudaSuccess) return cuda_fail(e, "fwd cluster launch");
+  } else {
+    kern<<<grid, T::THREADS, T::SMEM_BYTES, stream>>>(p, maps[0], maps[1], maps[2]);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "fwd launch");
+  }
   ++t_last_launches;
   return ELSA_OK;
+}
+
+// Clusters of `splits` CTAs of the cluster-merge kernel that fit the device at
+// once (cudaOccupancyMaxActiveClusters; a cluster must sit inside one GPC),
+// cached per configuration and split count; 0 when the size cannot launch.
+template <int W, int TK, int ST, int R>
+int max_active_clusters(int splits, DeviceCache* dc, int cfg_slot) {
+  using T = FwdTraits<W, TK, ST, R>;
+  int& cached = dc->clusters[cfg_slot][splits];
+  if (cached >= 0) return cached;
+  auto kern = fwd_f32_kernel<W, TK, ST, R, true, 64, 64, true>;
+  int n = 0;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(T::SMEM_BYTES)) == cudaSuccess &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+          cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, unsigned(splits), 1);
+    cfg.blockDim = dim3(T::THREADS);
+    cfg.dynamicSmemBytes = T::SMEM_BYTES;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = unsigned(splits);
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+  }
+  cudaGetLastError();  // a refused size is an answer, not an error state
+  cached = n;
+  return n;
 }
 
 int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[3],
                int64_t v_st[3], const Plan& plan, int64_t bh_count, DeviceCache* dc,
                cudaStream_t stream) {
   const int splits = plan.splits;
+  if (plan.cluster) {
+    if (plan.cfg == kCfgW8R8)
+      return launch_fwd_cfg<8, 64, ELSA_W8R8_STAGES, 8, 64, 64, true>(
+          p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8, dc, stream);
+    return launch_fwd_cfg<4, 64, ELSA_W4R8_STAGES, 8, 64, 64, true>(
+        p, s, q_st, k_st, v_st, splits, bh_count, kCfgW4R8, dc, stream);
+  }
   switch (plan.cfg) {
     case kCfgW8R16:
       return launch_fwd_cfg<8, 64, 2, 16>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R16, dc,
@@ -530,7 +697,7 @@ void fill_common(FwdParams& p, const float* q, const float* k, const float* v,
 }
 
 size_t split_ws_bytes(const elsa_shape* s, const Plan& pl) {
-  if (pl.splits <= 1) return 0;
+  if (pl.splits <= 1 || pl.cluster) return 0;
   const size_t rows = size_t(pl.heads_per_batch) * size_t(s->n_q);
   // m | S | (pad to 16 bytes) | W
   return size_t(pl.splits) * rows * size_t(2 + 64 * dv_slices(s->dv)) * sizeof(float) + 16;
@@ -580,8 +747,9 @@ int run_forward(const float* q, const float* k, const float* v, const elsa_shape
 
   const int64_t BH = shp->B * shp->H;
   const int64_t len = kv_end - kv_begin;
-  const Plan plan = force_plan ? *force_plan : plan_for(shp, len > 0 ? len : 1, kv_splits, dc->sms);
   const bool final_out = y != nullptr;
+  const Plan plan = force_plan ? *force_plan
+                               : plan_for(shp, len > 0 ? len : 1, kv_splits, dc->sms, final_out, dc);
   FwdParams p;
   fill_common(p, q, k, v, shp, scale, q_st, k_st, v_st);
   p.kv_begin = int(kv_begin);
@@ -594,6 +762,12 @@ int run_forward(const float* q, const float* k, const float* v, const elsa_shape
     p.ys_r = shp->y_stride[2];
     p.y_vec = (reinterpret_cast<uintptr_t>(y) % 16 == 0) && (p.ys_b % 4 == 0) &&
               (p.ys_h % 4 == 0) && (p.ys_r % 4 == 0);
+  }
+  if (plan.cluster && final_out) {
+    // one launch: the splits of each query tile form a cluster and merge over DSMEM
+    p.bh_begin = 0;
+    p.mode = kModeFinal;
+    return launch_fwd(p, shp, q_st, k_st, v_st, plan, BH, dc, strm);
   }
   if (plan.splits <= 1) {
     p.bh_begin = 0;
@@ -749,10 +923,10 @@ elsa_shape group_shape(const elsa_shape* s, int64_t cnt) {
   return g;
 }
 
-HostLayout host_layout(const elsa_shape* s, int kv_splits, int sms) {
+HostLayout host_layout(const elsa_shape* s, int kv_splits, int sms, DeviceCache* dc) {
   HostLayout L;
   const int64_t BH = s->B * s->H;
-  L.plan = plan_for(s, s->n_kv, kv_splits, sms);
+  L.plan = plan_for(s, s->n_kv, kv_splits, sms, true, dc);
   const int64_t g = BH < kPipeMaxGroups ? (BH > 0 ? BH : 1) : kPipeMaxGroups;
   L.hpg = ceil_div(BH > 0 ? BH : 1, g);
   L.groups = int(ceil_div(BH > 0 ? BH : 1, L.hpg));
@@ -811,7 +985,7 @@ int elsa_resolve_kv_splits(const elsa_shape* shp, int requested) {
   DeviceCache* dc = nullptr;
   int sms = 148;
   if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
-  return plan_for(shp, shp->n_kv, requested, sms).splits;
+  return plan_for(shp, shp->n_kv, requested, sms, true, dc).splits;
 }
 
 size_t elsa_workspace_bytes(const elsa_shape* shp, int kv_splits) {
@@ -819,8 +993,29 @@ size_t elsa_workspace_bytes(const elsa_shape* shp, int kv_splits) {
   DeviceCache* dc = nullptr;
   int sms = 148;
   if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
-  return split_ws_bytes(shp, plan_for(shp, shp->n_kv, kv_splits, sms));
+  return split_ws_bytes(shp, plan_for(shp, shp->n_kv, kv_splits, sms, true, dc));
 }
+
+size_t elsa_partial_workspace_bytes(const elsa_shape* shp, int64_t kv_begin, int64_t kv_end,
+                                    int kv_splits) {
+  if (!valid_shape(shp) || kv_splits < 0 || kv_begin < 0 || kv_end > shp->n_kv) return 0;
+  DeviceCache* dc = nullptr;
+  int sms = 148;
+  if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
+  const int64_t len = kv_end - kv_begin;
+  // partial states never use the cluster merge (its output is Y)
+  return split_ws_bytes(shp, plan_for(shp, len > 0 ? len : 1, kv_splits, sms, false, dc));
+}
+
+// Development aid: cudaOccupancyMaxActiveClusters of the cluster-merge kernel
+// (cfg 0 = w4r8, 2 = w8r8) for `splits`-CTA clusters on the current device.
+int elsa_dev_max_active_clusters(int cfg, int splits) {
+  DeviceCache* dc = nullptr;
+  if (current_device_cache(&dc) != ELSA_OK) return -1;
+  return active_clusters(cfg == kCfgW8R8 ? kCfgW8R8 : kCfgW4R8, splits, dc);
+}
+
+void elsa_dev_set_cluster(int mode) { g_cluster_mode = mode < 0 ? 0 : (mode > 2 ? 2 : mode); }
 
 int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
                  const elsa_shape* shp, double scale, int kv_splits, void* workspace,
@@ -839,7 +1034,7 @@ size_t elsa_host_workspace_bytes(const elsa_shape* shp, int kv_splits) {
   DeviceCache* dc = nullptr;
   int sms = 148;
   if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
-  return host_layout(shp, kv_splits, sms).total;
+  return host_layout(shp, kv_splits, sms, dc).total;
 }
 
 int elsa_fwd_f32_host(const float* q, const float* k, const float* v, float* y,
@@ -851,7 +1046,7 @@ int elsa_fwd_f32_host(const float* q, const float* k, const float* v, float* y,
   if (shp->B * shp->H * shp->n_q == 0) return ELSA_OK;
   DeviceCache* dc = nullptr;
   if (int st = current_device_cache(&dc)) return st;
-  const HostLayout L = host_layout(shp, kv_splits, dc->sms);
+  const HostLayout L = host_layout(shp, kv_splits, dc->sms, dc);
   if (!dev_workspace || ws_bytes < L.total) return ELSA_ERR_WORKSPACE;
   HostPipe* hp = nullptr;
   if (int st = host_pipe(&hp)) return st;
@@ -1302,7 +1497,7 @@ int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n
   DeviceCache* dc = nullptr;
   int sms = 148;
   if (current_device_cache(&dc) == ELSA_OK) sms = dc->sms;
-  const Plan pl = plan_for(shp, shp->n_kv, kv_splits, sms);
+  const Plan pl = plan_for(shp, shp->n_kv, kv_splits, sms, true, dc);
   static const char* names[] = {"w4r8",     "w8r16",        "w8r8",    "w8r8d128",
                                 "w8r8v128", "w8r8d128v128", "w8r8d96", "w8r8d96v128",
                                 "w8r8d256", "w4r8d256v128", "w8r8d32v32", "w8r8d96v96",
@@ -1313,6 +1508,7 @@ int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n
   const int64_t slices = ceil_div(shp->dv, cfg_dv(pl.cfg));
   const int64_t chain = ceil_div(ceil_div(shp->n_kv, ci.tk), pl.splits);
   std::string extra = slices > 1 ? " dv_slices=" + std::to_string(slices) : std::string();
+  if (pl.cluster) extra += " cluster_merge=dsmem";
   if (chain > kMaxChainTiles)
     extra += " chain_tiles=" + std::to_string(chain) + " (over the " +
              std::to_string(kMaxChainTiles) + "-tile cap: > kMaxSplits x cap keys)";

@@ -46,6 +46,9 @@
 #include <cstdint>
 #include <math_constants.h>
 
+#include <cooperative_groups.h>
+
+#include "merge_f32.cuh"
 #include "ptx.cuh"
 
 // Compile-time tuning knobs (defaults = the shipped configuration; the
@@ -238,6 +241,8 @@ struct FwdTraits {
   // straight into Q^T (kQtDirect; no TMA for such kernels).
   static constexpr bool kQtDirect = QRAW_FLOATS > P_FLOATS && QRAW_FLOATS > STAGES * K_FLOATS;
   static constexpr bool kQrawInK = QRAW_FLOATS > P_FLOATS && !kQtDirect;
+  // cluster merge: W[TQ][64] | m[TQ] | S[TQ] of the CTA's rows fit in its K/V ring
+  static constexpr bool kCluStateFits = size_t(TQ) * 66 <= size_t(STAGES) * (K_FLOATS + V_FLOATS);
   static constexpr size_t BAR_OFFSET =
       size_t(QT_FLOATS + STAGES * (K_FLOATS + V_FLOATS) + P_FLOATS) * 4;
   static constexpr size_t SMEM_BYTES = BAR_OFFSET + (2 * STAGES + 2) * 8;
@@ -326,17 +331,118 @@ __device__ __forceinline__ void producer_generic(const FwdParams& p, float* Qraw
   }
 }
 
+// Cluster-merge epilogue (fwd_f32_kernel<..., CL = true>). `st` is the CTA's
+// K/V ring, free once every consumer warp has folded its last tile: it holds
+// this CTA's states W[TQ][64] | m[TQ] | S[TQ] (log2 anchors, exactly the values
+// the split path writes to its workspace).
+template <class T, int MAXP>
+__device__ __forceinline__ void cluster_merge_rows(const FwdParams& p, float* st, int parts,
+                                                   int rank, int warp, int lane, int b, int h,
+                                                   int q0) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int TQ = T::TQ;
+  const int rpc = (TQ + parts - 1) / parts;  // rows this CTA finalizes
+  const int r0 = rank * rpc;
+  const int r1 = r0 + rpc < TQ ? r0 + rpc : TQ;
+  for (int lr = r0 + warp; lr < r1; lr += T::W) {
+    const int qrow = q0 + lr;
+    if (qrow >= p.n_q) break;
+    float am[MAXP], aS[MAXP], a0[MAXP], a1[MAXP];
+#pragma unroll
+    for (int i = 0; i < MAXP; ++i) {
+      if (i < parts) {
+        const float* peer = cluster.map_shared_rank(st, i);
+        am[i] = peer[TQ * 64 + lr];
+        aS[i] = peer[TQ * 65 + lr];
+        a0[i] = peer[lr * 64 + lane];
+        a1[i] = peer[lr * 64 + lane + 32];
+      } else {
+        am[i] = -CUDART_INF_F;
+        aS[i] = 0.f;
+        a0[i] = 0.f;
+        a1[i] = 0.f;
+      }
+    }
+    merge_tree_regs<MAXP>(am, aS, a0, a1, parts, true);
+    const float s = aS[0];
+    if (!(s > 0.f) || !isfinite(s)) {
+      if (lane == 0) atomicCAS(p.err, 0, 3);
+    }
+    float* yrow = p.y + int64_t(b) * p.ys_b + int64_t(h) * p.ys_h + int64_t(qrow) * p.ys_r;
+    if (lane < p.dv) yrow[lane] = __fdiv_rn(a0[0], s);
+    if (lane + 32 < p.dv) yrow[lane + 32] = __fdiv_rn(a1[0], s);
+  }
+}
+
+template <class T>
+__device__ __forceinline__ void cluster_merge_epilogue(const FwdParams& p, float* st,
+                                                       const float (&mrow)[T::R],
+                                                       const ptx::f32x2 (&l2)[T::RP],
+                                                       const ptx::f32x2 (&o2)[T::RP][T::CV],
+                                                       int warp, int lane, int rg, int g, int b,
+                                                       int h, int q0) {
+  namespace cg = cooperative_groups;
+  constexpr int TQ = T::TQ, R = T::R, RP = T::RP, WR = T::WR;
+  // every consumer warp is done reading the ring (its last GEMM2) before any
+  // warp overwrites it with states
+  asm volatile("bar.sync 1, %0;" ::"r"(T::W * 32) : "memory");
+#pragma unroll
+  for (int ip = 0; ip < RP; ++ip) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int i = 2 * ip + half;
+      float l = half ? ptx::hi2(l2[ip]) : ptx::lo2(l2[ip]);
+      l += __shfl_xor_sync(0xffffffffu, l, 1);
+      l += __shfl_xor_sync(0xffffffffu, l, 2);
+      l += __shfl_xor_sync(0xffffffffu, l, 4);
+      l += __shfl_xor_sync(0xffffffffu, l, 16);
+      const int lr = warp * WR + rg + 2 * i;
+      float4 w;
+      w.x = half ? ptx::hi2(o2[ip][0]) : ptx::lo2(o2[ip][0]);
+      w.y = half ? ptx::hi2(o2[ip][1]) : ptx::lo2(o2[ip][1]);
+      w.z = half ? ptx::hi2(o2[ip][2]) : ptx::lo2(o2[ip][2]);
+      w.w = half ? ptx::hi2(o2[ip][3]) : ptx::lo2(o2[ip][3]);
+      *reinterpret_cast<float4*>(st + lr * 64 + 4 * g) = w;
+      if (g == 0) {
+        st[TQ * 64 + lr] = mrow[i];
+        st[TQ * 65 + lr] = l;
+      }
+    }
+  }
+  (void)R;
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster.sync();  // release our states / acquire the peers'
+  const int parts = int(cluster.num_blocks());
+  const int rank = int(cluster.block_rank());
+  if (parts <= 8)
+    cluster_merge_rows<T, 8>(p, st, parts, rank, warp, lane, b, h, q0);
+  else
+    cluster_merge_rows<T, 16>(p, st, parts, rank, warp, lane, b, h, q0);
+  cluster.sync();  // peers are done reading our states before this CTA exits
+}
+
 __device__ __forceinline__ float f4(const float4& v, int c) {
   return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
-template <int W_, int TK_, int STAGES_, int R_, bool kTMA, int D_ = 64, int DV_ = 64>
+// CL (cluster split merge): the kv splits of one query tile are the CTAs of
+// one thread-block cluster (cluster dims (1, splits, 1)). Instead of writing
+// partial states to a global workspace for a second (K2) launch, each CTA
+// leaves its rows' (m, S, W) in its own shared memory; after a cluster
+// barrier CTA r merges rows [r * TQ / splits, ...) by reading every peer's
+// states over distributed shared memory (DSMEM) with K2's fixed tree, and
+// writes Y. Same states, same tree, same arithmetic as K1 + K2: bitwise equal.
+template <int W_, int TK_, int STAGES_, int R_, bool kTMA, int D_ = 64, int DV_ = 64,
+          bool CL = false>
 __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS))
     fwd_f32_kernel(const __grid_constant__ FwdParams p, const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV) {
   using T = FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>;
   static_assert(!(kTMA && T::kQtDirect), "direct Q^T needs the copy engine");
+  static_assert(!CL || (DV_ == 64 && !T::kRegSplit && T::kCluStateFits),
+                "cluster merge: one 64-column slice, every warp alive, states fit the ring");
   constexpr int TK = T::TK, QP = T::QP, QTP = T::QTP, VP = T::VP, PTP = T::PTP, RK = T::RK;
   constexpr int R = T::R, RP = T::RP, WR = T::WR;
   using ptx::f32x2;
@@ -409,6 +515,11 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
     } else {
       producer_generic<T>(p, Qraw, Qt, Ks, Vs, full, empty, qbar, qfree, b, h, q0, col0,
                           split_lo, ntiles, lane);
+    }
+    if constexpr (CL) {
+      // every thread of the cluster takes part in both cluster barriers
+      cooperative_groups::this_cluster().sync();  // peers' states written
+      cooperative_groups::this_cluster().sync();  // peers done reading ours
     }
     return;
   }
@@ -687,6 +798,11 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
     if (!lagged) gemm2_release(t);
   }
   if (lagged && ntiles > 0) gemm2_release(ntiles - 1);
+
+  if constexpr (CL) {
+    cluster_merge_epilogue<T>(p, Ks, mrow, l2, o2, warp, lane, rg, g, b, h, q0);
+    return;
+  }
 
   // ---------------- epilogue ----------------
 #pragma unroll
