@@ -311,9 +311,10 @@ class Ctx:
             # per-rank file (set before NCCL is loaded) and are echoed to stderr:
             # the evidence that N ranks formed one communicator (stdout stays
             # one JSON line)
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+                os.environ["NCCL_DEBUG"] = "INFO"
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-            os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/elsa_nccl.{os.getpid()}.log")
+            os.environ["NCCL_DEBUG_FILE"] = f"/tmp/elsa_nccl.{os.getpid()}.log"
         import torch
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
@@ -541,69 +542,113 @@ def e2e_block(args, ctx, elsa, hl):
 LONG = {"c4": ("C4", 1, 16, 65536), "c5": ("C5", 1, 8, 1 << 20)}
 
 
+def probe_exchange(args, ctx, edist):
+    """The KV-sharded exchange this node supports: the fused peer merge needs
+    symmetric (peer-mapped) memory between every pair of GPUs; a tiny
+    sharded problem is run with it on every rank and the ranks agree (MIN)
+    whether it worked, else the NCCL all_to_all exchange is used."""
+    torch = ctx.torch
+    want = edist.resolve_exchange(args.exchange, torch.empty(0, device=ctx.dev))
+    if not ctx.distributed or want != "peer":
+        return want, None
+    chunks = edist.DEFAULT_CHUNKS if ctx.world <= 8 and 8 % ctx.world == 0 else ctx.world
+    err = None
+    try:
+        g = torch.Generator(device=ctx.dev)
+        g.manual_seed(3)
+        q, k, v = (torch.randn(1, 2, 512, 64, device=ctx.dev, generator=g) for _ in range(3))
+        kl, vl, off = edist.shard_kv(k, v, ctx.rank, ctx.world, chunks)
+        edist.kv_sharded_attention(q, kl.contiguous(), vl.contiguous(), off, 512, chunks=chunks,
+                                   gather=False, exchange="peer")
+        torch.cuda.synchronize()
+        ok = torch.ones(1, device=ctx.dev)
+    except Exception as exc:  # noqa: BLE001
+        err = f"{type(exc).__name__}: {str(exc)[:160]}"
+        print(f"[bench rank {ctx.rank}] peer exchange unavailable ({err}); using NCCL",
+              file=sys.stderr)
+        ok = torch.zeros(1, device=ctx.dev)
+    ctx.dist.all_reduce(ok, op=ctx.dist.ReduceOp.MIN)
+    edist.release_peer_buffers()
+    return ("peer" if ok.item() > 0 else "nccl"), err
+
+
 def long_context(args, ctx, elsa, edist, spec_peak):
     """C4 / C5 at this N: the single-GPU forward at N = 1, KV-sharded over the
     ranks at N > 1 (strong scaling of the fixed problem)."""
     torch = ctx.torch
     out = []
     names = [x.strip() for x in args.long.split(",") if x.strip() and x.strip() != "none"]
+    exchange, probe_err = probe_exchange(args, ctx, edist) if names else (None, None)
     for key in names:
-        tag, B, H, n = LONG[key]
-        gen = torch.Generator(device=ctx.dev)
-        gen.manual_seed(64 + n % 977)
-        q = torch.randn(B, H, n, 64, device=ctx.dev, generator=gen)
-        k = torch.randn(B, H, n, 64, device=ctx.dev, generator=gen)
-        v = torch.randn(B, H, n, 64, device=ctx.dev, generator=gen)
-        fl = flops(B, H, n, n)
-        steps = 3 if key == "c4" else 1
-        launches = [0]
-        row = {"config": tag, "workload": f"{tag} FP32 attention B{B} H{H} n{n} d64 dv64",
-               "n_gpus": ctx.world, "scaling": "strong"}
-        if not ctx.distributed:
-            def step():
-                y = elsa.scaled_dot_product_attention(q, k, v)
-                launches[0] += elsa.last_launch_count()
-                return 0, y.reshape(-1, 64)
-            # C5 at N = 1 is a ~39 s step: warm it on the first 8192 query rows
-            # (same keys, same kernel); C4 warms on the full problem
-            if key == "c5":
-                elsa.scaled_dot_product_attention(q[:, :, :8192], k, v)
-            else:
-                step()
-            row["path"] = "single GPU: elsa_fwd_f32 (" + elsa.describe_plan(q, k, v) + ")"
-        else:
-            chunks = edist.DEFAULT_CHUNKS if ctx.world <= 8 and 8 % ctx.world == 0 else ctx.world
-            kl, vl, off = edist.shard_kv(k, v, ctx.rank, ctx.world, chunks)
-            kl, vl = kl.contiguous(), vl.contiguous()
-            ex = [args.exchange]
-
-            def step():
-                r = edist.kv_sharded_attention(q, kl, vl, off, n, chunks=chunks, gather=False,
-                                               exchange=ex[0])
-                launches[0] += edist.last_launch_count()
-                return r
-            step()  # full warm-up: rendezvous of the peer buffer, workspaces
-            row["path"] = (f"KV-sharded: {chunks} global key chunks, {chunks // ctx.world} per "
-                           f"rank, exchange={args.exchange}")
-            row["per_rank_keys"] = int(kl.shape[2])
-        torch.cuda.synchronize()
-        launches[0] = 0
-        ms, (lo, y_rows) = ctx.timed(step, steps)
-        tf = fl / (ms * 1e-3) / 1e12
-        row.update({"steps": steps, "ms_per_step": ms, "value": tf, "unit": "TFLOP/s",
-                    "gpu_launches_per_step": ctx.max_over_ranks(launches[0]) / steps,
-                    "frac_ffma_peak_per_gpu": tf / (ctx.world * spec_peak)})
-        if not args.no_parity:
-            err, cnt = sampled_parity(q, k, v, y_rows, lo, 8 if key == "c5" else 16,
-                                      seed=100 + ctx.rank)
-            row["parity"] = _parity_block(ctx, err, cnt, n)
-        out.append(row)
-        del q, k, v, y_rows
-        if ctx.distributed:
-            del kl, vl
-            edist.release_peer_buffers()
-        torch.cuda.empty_cache()
+        try:
+            out.append(_long_one(args, ctx, elsa, edist, spec_peak, key, exchange, probe_err))
+        except Exception as exc:  # noqa: BLE001 - keep the headline line alive
+            print(f"[bench rank {ctx.rank}] long-context {key} failed: {exc}", file=sys.stderr)
+            out.append({"config": LONG[key][0], "error": f"{type(exc).__name__}: {str(exc)[:200]}"})
+            torch.cuda.empty_cache()
     return out
+
+
+def _long_one(args, ctx, elsa, edist, spec_peak, key, exchange, probe_err):
+    torch = ctx.torch
+    tag, B, H, n = LONG[key]
+    gen = torch.Generator(device=ctx.dev)
+    gen.manual_seed(64 + n % 977)
+    q = torch.randn(B, H, n, 64, device=ctx.dev, generator=gen)
+    k = torch.randn(B, H, n, 64, device=ctx.dev, generator=gen)
+    v = torch.randn(B, H, n, 64, device=ctx.dev, generator=gen)
+    fl = flops(B, H, n, n)
+    steps = 3 if key == "c4" else 1
+    launches = [0]
+    row = {"config": tag, "workload": f"{tag} FP32 attention B{B} H{H} n{n} d64 dv64",
+           "n_gpus": ctx.world, "scaling": "strong"}
+    if not ctx.distributed:
+        def step():
+            y = elsa.scaled_dot_product_attention(q, k, v)
+            launches[0] += elsa.last_launch_count()
+            return 0, y.reshape(-1, 64)
+        # C5 at N = 1 is a ~39 s step: warm it on the first 8192 query rows
+        # (same keys, same kernel); C4 warms on the full problem
+        if key == "c5":
+            elsa.scaled_dot_product_attention(q[:, :, :8192], k, v)
+        else:
+            step()
+        row["path"] = "single GPU: elsa_fwd_f32 (" + elsa.describe_plan(q, k, v) + ")"
+    else:
+        chunks = edist.DEFAULT_CHUNKS if ctx.world <= 8 and 8 % ctx.world == 0 else ctx.world
+        kl, vl, off = edist.shard_kv(k, v, ctx.rank, ctx.world, chunks)
+        kl, vl = kl.contiguous(), vl.contiguous()
+        ex = [exchange]
+
+        def step():
+            r = edist.kv_sharded_attention(q, kl, vl, off, n, chunks=chunks, gather=False,
+                                           exchange=ex[0])
+            launches[0] += edist.last_launch_count()
+            return r
+        step()  # full warm-up: rendezvous of the peer buffer, workspaces
+        row["path"] = (f"KV-sharded: {chunks} global key chunks, {chunks // ctx.world} per "
+                       f"rank, exchange={exchange}"
+                       + (f" (peer probe failed: {probe_err})" if probe_err else ""))
+        row["per_rank_keys"] = int(kl.shape[2])
+    torch.cuda.synchronize()
+    launches[0] = 0
+    ms, (lo, y_rows) = ctx.timed(step, steps)
+    tf = fl / (ms * 1e-3) / 1e12
+    row.update({"steps": steps, "ms_per_step": ms, "value": tf, "unit": "TFLOP/s",
+                "gpu_launches_per_step": ctx.max_over_ranks(launches[0]) / steps,
+                "frac_ffma_peak_per_gpu": tf / (ctx.world * spec_peak)})
+    if not args.no_parity:
+        err, cnt = sampled_parity(q, k, v, y_rows, lo, 8 if key == "c5" else 16,
+                                  seed=100 + ctx.rank)
+        row["parity"] = _parity_block(ctx, err, cnt, n)
+    del q, k, v, y_rows
+    if ctx.distributed:
+        del kl, vl
+        edist.release_peer_buffers()
+    torch.cuda.empty_cache()
+    return row
+
+
 
 
 def sweep_block(args, ctx, elsa, hl, spec_peak):

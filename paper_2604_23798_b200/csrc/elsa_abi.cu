@@ -646,7 +646,9 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
   }
 }
 
-int launch_merge(MergeParams& mp, cudaStream_t stream) {
+// pdl: launch as the preceding forward kernel's programmatic dependent
+// (its CTAs become resident while K1 drains; they start merging when K1 is done)
+int launch_merge(MergeParams& mp, cudaStream_t stream, bool pdl = false) {
   if (mp.rows == 0) return ELSA_OK;
   constexpr int kWarps = 8;
   const int64_t blocks = ceil_div(mp.rows, kWarps);
@@ -657,8 +659,24 @@ int launch_merge(MergeParams& mp, cudaStream_t stream) {
               : mp.parts <= 8  ? merge_f32_kernel<8>
               : mp.parts <= 16 ? merge_f32_kernel<16>
                                : merge_f32_kernel<32>;
-  kern<<<grid, kWarps * 32, 0, stream>>>(mp);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "merge launch");
+  static const bool no_pdl = std::getenv("ELSA_NO_PDL") != nullptr;  // A/B switch
+  if (pdl && !no_pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kWarps * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mp);
+    if (e != cudaSuccess) return cuda_fail(e, "merge launch (PDL)");
+  } else {
+    kern<<<grid, kWarps * 32, 0, stream>>>(mp);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail(cudaGetLastError(), "merge launch");
+  }
   ++t_last_launches;
   return ELSA_OK;
 }
@@ -831,7 +849,7 @@ int run_forward(const float* q, const float* k, const float* v, const elsa_shape
       mp.out_pitch = int(shp->dv);
       mp.out_log2_to_nat = 1;
     }
-    if (int st = launch_merge(mp, strm)) return st;
+    if (int st = launch_merge(mp, strm, true)) return st;
   }
   return ELSA_OK;
 }

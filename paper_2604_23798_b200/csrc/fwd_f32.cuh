@@ -477,6 +477,9 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   const int ntiles = kv_hi > split_lo ? (kv_hi - split_lo + TK - 1) / TK : 0;
 
   trace_cta(p, 0);
+  // a K2 merge launched as this grid's programmatic dependent may start its
+  // CTAs now (they wait in griddepcontrol.wait for this grid's completion)
+  ptx::griddep_launch_dependents();
   if (threadIdx.x == 0) {
     // TMA: one arrive.expect_tx per stage; copy engine: one arrival per lane
     for (int s = 0; s < T::STAGES; ++s) {

@@ -91,6 +91,9 @@ __device__ __forceinline__ void merge_tree_regs(float (&am)[MAXP], float (&aS)[M
 
 template <int MAXP>
 __global__ void __launch_bounds__(256) merge_f32_kernel(const MergeParams p) {
+  // launched as K1's programmatic dependent: the partial states are complete
+  // and visible once the forward grid has finished
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= p.rows) return;

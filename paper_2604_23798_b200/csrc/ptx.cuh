@@ -180,5 +180,15 @@ __device__ __forceinline__ void lds128x2(const float* p, f32x2& a, f32x2& b) {
   b = v.y;
 }
 
+// Programmatic dependent launch (sm_90+): the primary grid lets a dependent
+// grid launched with cudaLaunchAttributeProgrammaticStreamSerialization start
+// early; the dependent blocks in griddep_wait until the primary completed and
+// its memory is visible (a no-op for grids launched without the attribute).
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace ptx
+
 }  // namespace elsa
