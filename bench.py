@@ -134,6 +134,15 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout):
+        """Block until the sampler produced two samples (NVML initialised and
+        polling), then drop them: only samples of the timed region count."""
+        t0 = time.time()
+        while self.proc is not None and len(self.lines) < 2 and time.time() - t0 < timeout:
+            time.sleep(0.02)
+        time.sleep(0.1)
+        del self.lines[:]
+
     def stop(self):
         if self.proc is None:
             return None
@@ -471,12 +480,16 @@ def headline(args, ctx, elsa, edist):
             return r
 
     warm = max(args.warmup, 3)
+    # the sampler starts before the warm-up: on a fresh box nvidia-smi's first
+    # NVML initialisation stalls the GPU for milliseconds (measured: the first
+    # bench run on a box 22.8 ms/step, the next ones 19.18), so it must be
+    # sampling steadily before the timed region opens
+    clocks = ClockSampler(ctx.local)
+    clocks.start()
     for _ in range(warm):
         step()
     torch.cuda.synchronize()
-    clocks = ClockSampler(ctx.local)
-    clocks.start()
-    time.sleep(0.15)
+    clocks.wait_first(timeout=10.0)
     launches[0] = 0
     ms, (lo, y_rows) = ctx.timed(step, args.steps)
     clock_info = clocks.stop()
