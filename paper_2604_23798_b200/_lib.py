@@ -97,6 +97,9 @@ def _declare(h):
     if hasattr(h, "elsa_dev_set_cluster"):
         h.elsa_dev_set_cluster.restype = None
         h.elsa_dev_set_cluster.argtypes = [c_int]
+    if hasattr(h, "elsa_dev_force_config"):
+        h.elsa_dev_force_config.restype = None
+        h.elsa_dev_force_config.argtypes = [ctypes.c_char_p]
     h.elsa_fwd_f32.restype = c_int
     h.elsa_fwd_f32.argtypes = [c_vp, c_vp, c_vp, c_vp, shp, c_dbl, c_int, c_vp, c_sz, c_vp]
     h.elsa_host_workspace_bytes.restype = c_sz

@@ -648,6 +648,18 @@ def set_cluster_mode(mode):
     _FAST.clear()
 
 
+def force_config(name=None):
+    """Development aid: force one of the d <= 64 kernel configurations
+    ("w4r8", "w8r8", "w8r16", or "w8r8acc", the two-level-accumulator kernel
+    for long per-CTA chains); None restores the planner's choice."""
+    h = _lib.lib()
+    if not hasattr(h, "elsa_dev_force_config"):
+        raise ShapeError("this libelsa build has no configuration control")
+    h.elsa_dev_force_config(name.encode() if name else None)
+    _SHAPE_CACHE.clear()
+    _FAST.clear()
+
+
 def ffma_peak_tflops(device=None):
     """Run the K4 FFMA microbenchmark on ``device`` and return TFLOP/s."""
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device

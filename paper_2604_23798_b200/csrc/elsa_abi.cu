@@ -43,7 +43,7 @@ constexpr int kMaxDevices = 64;
 #ifndef ELSA_W4R8_STAGES
 #define ELSA_W4R8_STAGES 2
 #endif
-constexpr int kAttrSlots = 38;
+constexpr int kAttrSlots = 40;
 constexpr int kMaxSplits = kMergeMaxParts;
 constexpr double kLog2e = 1.4426950408889634074;
 
@@ -154,6 +154,7 @@ enum CfgId {
   kCfgW8R8V96 = 12,     // d <= 64 < dv <= 96
   kCfgW8R8D128V96 = 13, // 96 < d <= 128, 64 < dv <= 96
   kCfgW4R8D256V256 = 14,  // 128 < d <= 256, dv > 128: 256 V columns per CTA (one S per tile)
+  kCfgW8R8Acc = 15,  // w8r8 with the two-level W accumulator (long per-CTA chains)
   kCfgAuto = -1
 };
 int cfg_dv(int cfg) {
@@ -180,16 +181,16 @@ constexpr int64_t kMaxD = 256;
 constexpr int64_t kMaxDv = 4096;
 int64_t dv_slices(int64_t dv) { return (dv + 63) / 64; }
 
-int forced_cfg() {
-  static int cfg = [] {
-    const char* e = std::getenv("ELSA_FWD_CFG");
-    if (e && !std::strcmp(e, "w4r8")) return int(kCfgW4R8);
-    if (e && !std::strcmp(e, "w8r8")) return int(kCfgW8R8);
-    if (e && !std::strcmp(e, "w8r16")) return int(kCfgW8R16);
-    return int(kCfgAuto);
-  }();
-  return cfg;
+int cfg_from_name(const char* e) {
+  if (e && !std::strcmp(e, "w4r8")) return int(kCfgW4R8);
+  if (e && !std::strcmp(e, "w8r8")) return int(kCfgW8R8);
+  if (e && !std::strcmp(e, "w8r16")) return int(kCfgW8R16);
+  if (e && !std::strcmp(e, "w8r8acc")) return int(kCfgW8R8Acc);
+  return int(kCfgAuto);
 }
+// ELSA_FWD_CFG (or elsa_dev_force_config) forces one of the d <= 64 configurations
+int g_forced_cfg = cfg_from_name(std::getenv("ELSA_FWD_CFG"));
+int forced_cfg() { return g_forced_cfg; }
 
 struct CfgInfo {
   int tq, tk, ctas_per_sm;
@@ -206,6 +207,8 @@ CfgInfo cfg_info(int cfg) {
       return {256, 64, 1, 10.75, 7.6};
     case kCfgW8R8:
       return {128, 64, 1, 5.355, 4.1};
+    case kCfgW8R8Acc:  // ~1% more per tile than w8r8 (profiles/round2_ab_acc.txt)
+      return {128, 64, 1, 5.41, 4.1};
     // wide-head configurations: scaled from the w8r8 fit by GEMM length
     // (d + dv relative to 128), not fitted — the planner only compares kv
     // split counts within one of them
@@ -262,7 +265,12 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // tiles sequentially (bounded chain depth; the rest is the log-depth tree).
 // 1024 tiles: chains of ~1100 tiles measured 5.5e-6 at 1M (bound 1.7e-5) and
 // 4.0e-6 at 64K (bound 1.3e-5); 16384 measured 2.5e-5 (over).
+// The two-level-accumulator kernel (kCfgW8R8Acc) rounds each W element over
+// 64 keys + one step per tile: one 16384-tile chain measured 3.1e-6 at 1M
+// (0.18 x bound; profiles/round2_chain_error_acc.txt), so its cap is 16384.
 constexpr int64_t kMaxChainTiles = 1024;
+constexpr int64_t kMaxChainTilesAcc = 16384;
+int64_t chain_cap(int cfg) { return cfg == kCfgW8R8Acc ? kMaxChainTilesAcc : kMaxChainTiles; }
 // Split workspace budget for auto planning (partial states are
 // (2 + 64 * dv slices) * 4 B per row per split): 4 GiB unless ELSA_MAX_WORKSPACE_MB says
 // otherwise. Explicit kv_splits requests are not capped.
@@ -332,13 +340,15 @@ Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms,
   // head widths beyond 64 have one configuration each; d, dv <= 64 choose
   const int only = wide_cfg(sh->d, sh->dv);
   const bool wide = only >= 0;
-  const int first = wide ? only : 0, last = wide ? only + 1 : int(kCfgCount);
+  const int first = wide ? only : 0, last = wide ? only + 1 : int(kCfgCount) + 1;
   Plan best{first, 1, BH > 0 ? BH : 1};
   double best_t = 1e300;
   const int forced = wide ? int(kCfgAuto) : forced_cfg();
   const int64_t slices = ceil_div(sh->dv, cfg_dv(first));
   const int64_t head_bytes = sh->n_q * (2 + 64 * dv_slices(sh->dv)) * 4;  // one split of one (b, h) head
-  for (int cfg = first; cfg < last; ++cfg) {
+  for (int ci_ = first; ci_ < last; ++ci_) {
+    // d, dv <= 64: w4r8, w8r16, w8r8, then the long-chain w8r8acc
+    const int cfg = (!wide && ci_ == int(kCfgCount)) ? int(kCfgW8R8Acc) : ci_;
     if (forced != kCfgAuto && cfg != forced) continue;
     const CfgInfo ci = cfg_info(cfg);
     const int64_t ctas = ceil_div(sh->n_q, ci.tq) * BH * slices;
@@ -355,7 +365,7 @@ Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms,
       // workspace then exceeds the soft budget for a single head); beyond
       // kMaxSplits * kMaxChainTiles tiles the chain grows and describe_plan
       // reports it
-      lo = ceil_div(tiles, kMaxChainTiles);
+      lo = ceil_div(tiles, chain_cap(cfg));
       if (lo > hi) lo = hi;
       const int64_t ws_cap = head_bytes > 0 ? workspace_budget() / head_bytes : hi;
       if (hi > ws_cap) hi = ws_cap < lo ? lo : ws_cap;
@@ -369,7 +379,11 @@ Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms,
         if (hpb > BH) hpb = BH;
       }
       const int64_t batches = ceil_div(BH, hpb);
-      const double t = plan_cost(ci, ctas, tiles, rows, sms, sn) + 8.0 * double(batches - 1);
+      double t = plan_cost(ci, ctas, tiles, rows, sms, sn) + 8.0 * double(batches - 1);
+      // a chain over the config's cap (only past kMaxSplits x cap tiles) is
+      // an accuracy cost: prefer the config whose cap it exceeds least
+      const int64_t chain = ceil_div(tiles, sn);
+      if (chain > chain_cap(cfg)) t *= 1.0 + double(chain) / double(chain_cap(cfg));
       if (t < best_t - 1e-9) {
         best_t = t;
         best = Plan{cfg, int(sn), hpb};
@@ -475,7 +489,8 @@ bool encode_map_uncached(CUtensorMap* map, const float* base, int64_t inner, int
   return r == CUDA_SUCCESS;
 }
 
-template <int W, int TK, int ST, int R, int D = 64, int DV = 64, bool CL = false>
+template <int W, int TK, int ST, int R, int D = 64, int DV = 64, bool CL = false,
+          bool ACC = false>
 int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[3],
                    int64_t v_st[3], int splits, int64_t bh_count, int cfg_slot, DeviceCache* dc,
                    cudaStream_t stream) {
@@ -505,9 +520,9 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
   static const bool force_generic = std::getenv("ELSA_FORCE_GENERIC_LOAD") != nullptr;
   if (force_generic) use_tma = false;
 
-  auto kern = fwd_f32_kernel<W, TK, ST, R, false, D, DV, CL>;
+  auto kern = fwd_f32_kernel<W, TK, ST, R, false, D, DV, CL, ACC>;
   if constexpr (T::QP <= 256) {
-    if (use_tma) kern = fwd_f32_kernel<W, TK, ST, R, true, D, DV, CL>;
+    if (use_tma) kern = fwd_f32_kernel<W, TK, ST, R, true, D, DV, CL, ACC>;
   }
   const int slot = (CL ? kCluAttrBase : 0) + cfg_slot * 2 + (use_tma ? 1 : 0);
   if (!dc->attr[slot]) {
@@ -604,6 +619,9 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
     case kCfgW8R8:
       return launch_fwd_cfg<8, 64, ELSA_W8R8_STAGES, 8>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8, dc,
                                          stream);
+    case kCfgW8R8Acc:
+      return launch_fwd_cfg<8, 64, ELSA_W8R8_STAGES, 8, 64, 64, false, true>(
+          p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8Acc, dc, stream);
     case kCfgW8R8D128:
       return launch_fwd_cfg<8, 64, 2, 8, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
                                               kCfgW8R8D128, dc, stream);
@@ -1034,6 +1052,10 @@ int elsa_dev_max_active_clusters(int cfg, int splits) {
 }
 
 void elsa_dev_set_cluster(int mode) { g_cluster_mode = mode < 0 ? 0 : (mode > 2 ? 2 : mode); }
+
+// Development aid: force a d <= 64 configuration by name ("w4r8", "w8r8",
+// "w8r16", "w8r8acc"; anything else = the planner's choice).
+void elsa_dev_force_config(const char* name) { g_forced_cfg = cfg_from_name(name); }
 
 int elsa_fwd_f32(const float* q, const float* k, const float* v, float* y,
                  const elsa_shape* shp, double scale, int kv_splits, void* workspace,
@@ -1519,17 +1541,17 @@ int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n
   static const char* names[] = {"w4r8",     "w8r16",        "w8r8",    "w8r8d128",
                                 "w8r8v128", "w8r8d128v128", "w8r8d96", "w8r8d96v128",
                                 "w8r8d256", "w4r8d256v128", "w8r8d32v32", "w8r8d96v96",
-                                "w8r8v96", "w8r8d128v96", "w4r8d256v256"};
-  static_assert(sizeof(names) / sizeof(names[0]) == kCfgW4R8D256V256 + 1, "one name per config");
-  if (pl.cfg < 0 || pl.cfg > kCfgW4R8D256V256) return ELSA_ERR_SHAPE;
+                                "w8r8v96", "w8r8d128v96", "w4r8d256v256", "w8r8acc"};
+  static_assert(sizeof(names) / sizeof(names[0]) == kCfgW8R8Acc + 1, "one name per config");
+  if (pl.cfg < 0 || pl.cfg > kCfgW8R8Acc) return ELSA_ERR_SHAPE;
   const CfgInfo ci = cfg_info(pl.cfg);
   const int64_t slices = ceil_div(shp->dv, cfg_dv(pl.cfg));
   const int64_t chain = ceil_div(ceil_div(shp->n_kv, ci.tk), pl.splits);
   std::string extra = slices > 1 ? " dv_slices=" + std::to_string(slices) : std::string();
   if (pl.cluster) extra += " cluster_merge=dsmem";
-  if (chain > kMaxChainTiles)
+  if (chain > chain_cap(pl.cfg))
     extra += " chain_tiles=" + std::to_string(chain) + " (over the " +
-             std::to_string(kMaxChainTiles) + "-tile cap: > kMaxSplits x cap keys)";
+             std::to_string(chain_cap(pl.cfg)) + "-tile cap: > kMaxSplits x cap keys)";
   std::snprintf(buf, n, "%s tq=%d tk=%d kv_splits=%d heads_per_batch=%lld%s", names[pl.cfg],
                 ci.tq, ci.tk, pl.splits, static_cast<long long>(pl.heads_per_batch),
                 extra.c_str());

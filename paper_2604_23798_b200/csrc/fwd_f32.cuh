@@ -433,8 +433,17 @@ __device__ __forceinline__ float f4(const float4& v, int c) {
 // barrier CTA r merges rows [r * TQ / splits, ...) by reading every peer's
 // states over distributed shared memory (DSMEM) with K2's fixed tree, and
 // writes Y. Same states, same tree, same arithmetic as K1 + K2: bitwise equal.
+// ACC (the long-chain kernels): two-level W accumulation. Each tile's P V
+// goes into a fresh accumulator that is folded into the running W once per
+// tile (W = W * corr + W_t, one FFMA2 in place of the rescale's FMUL2), so
+// every W element's sequential rounding chain is TK keys inside the tile plus
+// one step per tile, instead of every key the CTA folds. Measured at 1M keys
+// with one 16384-tile chain: max row error 3.1e-6 vs 2.6e-5 without
+// (profiles/round2_chain_error_acc.txt); ~1% slower per tile, so the planner
+// uses it where chains are long (it then needs no kv splits for the error
+// bound).
 template <int W_, int TK_, int STAGES_, int R_, bool kTMA, int D_ = 64, int DV_ = 64,
-          bool CL = false>
+          bool CL = false, bool ACC = false>
 __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS))
     fwd_f32_kernel(const __grid_constant__ FwdParams p, const __grid_constant__ CUtensorMap tmQ,
                    const __grid_constant__ CUtensorMap tmK,
@@ -589,6 +598,11 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   f32x2 o2[RP][CV];  // W accumulator: [row pair][column VW g + 16 VW (c / VW) + c % VW]
   float mrow[R];    // running anchors (log2 units)
   f32x2 l2[RP];     // running normalizer partials (this lane's keys)
+  // ELSA_TILE_ACC: this tile's P V (t2) and the running side's factor (corr_t)
+  constexpr bool kTileAcc = ACC && CV <= 8;  // V slices of <= 128 columns
+  static_assert(!(kTileAcc && T::kLag), "per-tile accumulation assumes the in-order GEMM2");
+  f32x2 t2[RP][kTileAcc ? CV : 1];
+  f32x2 corr_t[RP];
 #pragma unroll
   for (int ip = 0; ip < RP; ++ip) {
     l2[ip] = 0ull;
@@ -604,6 +618,14 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   auto gemm2 = [&](int tt, int k0) {
     const int st = tt % T::STAGES;
     const float* vs = Vs + st * T::V_FLOATS;
+    if constexpr (kTileAcc) {
+      if (k0 == 0) {
+#pragma unroll
+        for (int ip = 0; ip < RP; ++ip)
+#pragma unroll
+          for (int c = 0; c < CV; ++c) t2[ip][c] = 0ull;
+      }
+    }
 #pragma unroll(T::G2_UNROLL)
     for (int jj = 0; jj < TK / T::PH; ++jj) {
       f32x2 pr[RP];
@@ -630,7 +652,10 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
 #pragma unroll
         for (int u = 0; u < RP; ++u) {
           const int ip = (ELSA_SNAKE && (c & 1)) ? RP - 1 - u : u;
-          ptx::ffma2(o2[ip][c], vb, pr[ip]);
+          if constexpr (kTileAcc)
+            ptx::ffma2(t2[ip][kTileAcc ? c : 0], vb, pr[ip]);
+          else
+            ptx::ffma2(o2[ip][c], vb, pr[ip]);
         }
       }
     }
@@ -642,8 +667,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
       // the d <= 64 / dv <= 64 kernels: this exact form (ptxas schedules the
       // generalised loop differently)
       const float* vs = Vs + st * T::V_FLOATS + 4 * g;
-#pragma unroll(T::G2_UNROLL)
-      for (int jj = 0; jj < TK; ++jj) {
+      auto key_step = [&](int jj, bool first) {
         f32x2 pr[RP];
 #pragma unroll
         for (int u = 0; u < RP / 2; ++u)
@@ -656,12 +680,38 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
 #pragma unroll
           for (int u = 0; u < RP; ++u) {
             const int ip = (ELSA_SNAKE && (c & 1)) ? RP - 1 - u : u;
-            ptx::ffma2(o2[ip][c], vb, pr[ip]);
+            if constexpr (kTileAcc) {
+              if (first)
+                t2[ip][c] = ptx::fmul2(vb, pr[ip]);
+              else
+                ptx::ffma2(t2[ip][c], vb, pr[ip]);
+            } else {
+              ptx::ffma2(o2[ip][c], vb, pr[ip]);
+            }
           }
         }
+      };
+      if constexpr (kTileAcc) {
+        // the tile accumulator starts at the first key's products (no zeroing):
+        // one peeled block of G2_UNROLL keys, then the unrolled loop
+#pragma unroll
+        for (int jj = 0; jj < T::G2_UNROLL; ++jj) key_step(jj, jj == 0);
+#pragma unroll(T::G2_UNROLL)
+        for (int jj = T::G2_UNROLL; jj < TK; ++jj) key_step(jj, false);
+      } else {
+#pragma unroll(T::G2_UNROLL)
+        for (int jj = 0; jj < TK; ++jj) key_step(jj, false);
       }
     } else {
       gemm2(tt, (T::PH - 1) * (TK / T::PH));
+    }
+    if constexpr (kTileAcc) {
+      // fold the tile into the running W: W = W * corr + W_t
+#pragma unroll
+      for (int ip = 0; ip < RP; ++ip)
+#pragma unroll
+        for (int c = 0; c < CV; ++c)
+          o2[ip][c] = ptx::ffma2r(o2[ip][c], corr_t[ip], t2[ip][kTileAcc ? c : 0]);
     }
     __syncwarp();
     trace_mark(p, warp, tt, 4);
@@ -774,8 +824,12 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
         ps = j == 0 ? s2[ip][j] : ptx::fadd2(ps, s2[ip][j]);
       }
       l2[ip] = ptx::ffma2r(l2[ip], corr, ps);
+      if constexpr (kTileAcc) {
+        corr_t[ip] = corr;
+      } else {
 #pragma unroll
-      for (int c = 0; c < CV; ++c) o2[ip][c] = ptx::fmul2(o2[ip][c], corr);
+        for (int c = 0; c < CV; ++c) o2[ip][c] = ptx::fmul2(o2[ip][c], corr);
+      }
     }
     if constexpr (T::kHalfP) {
       // first key half through the (half-size) P area, then the second half

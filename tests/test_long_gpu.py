@@ -110,11 +110,20 @@ def test_c5_kv_sharded_peer_and_nccl(c5, pg):
 def test_chain_cap_holds_when_workspace_budget_binds():
     """A 2^20-row head at 2^20 keys: the 4 GiB split-workspace budget alone
     would allow 15 splits (a 1093-tile chain); the planner keeps the chain
-    cap (>= 16 splits) and the workspace grows past the soft budget. Beyond
-    kMaxSplits x 1024 tiles the over-long chain is reported by describe_plan."""
+    cap of the config it picks (1024 tiles for w8r8, 16384 for the two-level
+    accumulator kernel w8r8acc) and the workspace grows past the soft budget.
+    Beyond kMaxSplits x cap tiles the over-long chain is reported by
+    describe_plan."""
     q = torch.empty(1, 1, N_KV, 64, device=DEV)
     plan = elsa.describe_plan(q, q, q)
-    assert elsa.resolve_kv_splits(q, q, q) >= 16 and "chain_tiles" not in plan, plan
+    splits = elsa.resolve_kv_splits(q, q, q)
+    cap = 16384 if plan.startswith("w8r8acc") else 1024
+    assert -(-(N_KV // 64) // splits) <= cap and "chain_tiles" not in plan, plan
     kk = torch.empty(1, 1, 1 << 22, 64, device=DEV)   # 65536 tiles > 32 x 1024
     plan = elsa.describe_plan(q[:, :, :1024], kk, kk)
-    assert "chain_tiles=2048" in plan, plan
+    assert plan.startswith("w8r8acc") and "chain_tiles" not in plan, plan
+    # 2^26 keys = 2^20 tiles > 32 x 16384: the chain grows and is reported
+    # (a stride-0 view: the planner needs shapes only)
+    big = torch.empty(1, 1, 1, 64, device=DEV).expand(1, 1, 1 << 26, 64)
+    plan = elsa.describe_plan(q[:, :, :1024], big, big)
+    assert "chain_tiles=32768" in plan, plan
