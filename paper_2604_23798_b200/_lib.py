@@ -97,6 +97,9 @@ def _declare(h):
     if hasattr(h, "elsa_dev_set_cluster"):
         h.elsa_dev_set_cluster.restype = None
         h.elsa_dev_set_cluster.argtypes = [c_int]
+    if hasattr(h, "elsa_dev_set_tail"):
+        h.elsa_dev_set_tail.restype = None
+        h.elsa_dev_set_tail.argtypes = [c_int]
     if hasattr(h, "elsa_dev_force_config"):
         h.elsa_dev_force_config.restype = None
         h.elsa_dev_force_config.argtypes = [ctypes.c_char_p]

@@ -648,6 +648,17 @@ def set_cluster_mode(mode):
     _FAST.clear()
 
 
+def set_tail_mode(mode):
+    """Development aid: tail split of a one-split plan's last wave (0 = off,
+    1 = the measured rule, s >= 2 = force s key pieces per tail unit)."""
+    h = _lib.lib()
+    if not hasattr(h, "elsa_dev_set_tail"):
+        raise ShapeError("this libelsa build has no tail-split control")
+    h.elsa_dev_set_tail(int(mode))
+    _SHAPE_CACHE.clear()
+    _FAST.clear()
+
+
 def force_config(name=None):
     """Development aid: force one of the d <= 64 kernel configurations
     ("w4r8", "w8r8", "w8r16", or "w8r8acc", the two-level-accumulator kernel

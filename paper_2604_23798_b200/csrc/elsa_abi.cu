@@ -43,7 +43,7 @@ constexpr int kMaxDevices = 64;
 #ifndef ELSA_W4R8_STAGES
 #define ELSA_W4R8_STAGES 2
 #endif
-constexpr int kAttrSlots = 40;
+constexpr int kAttrSlots = 42;
 constexpr int kMaxSplits = kMergeMaxParts;
 constexpr double kLog2e = 1.4426950408889634074;
 
@@ -75,7 +75,7 @@ struct DeviceCache {
   int sms = 0;
   int* err = nullptr;
   bool attr[2 * kAttrSlots] = {};  // forward configs x TMA flag, then the tc kernels; cluster kernels
-  int clusters[2][17];             // max active clusters: [w4r8, w8r8][splits], -1 = unknown
+  int clusters[3][17];             // max active clusters: [w4r8, w8r8, w8r4][splits], -1 = unknown
   DeviceCache() {
     for (auto& row : clusters)
       for (int& x : row) x = -1;
@@ -155,6 +155,7 @@ enum CfgId {
   kCfgW8R8D128V96 = 13, // 96 < d <= 128, 64 < dv <= 96
   kCfgW4R8D256V256 = 14,  // 128 < d <= 256, dv > 128: 256 V columns per CTA (one S per tile)
   kCfgW8R8Acc = 15,  // w8r8 with the two-level W accumulator (long per-CTA chains)
+  kCfgW8R4 = 16,     // 8 consumer warps x 8 rows (TQ 64): latency-bound small problems
   kCfgAuto = -1
 };
 int cfg_dv(int cfg) {
@@ -186,6 +187,7 @@ int cfg_from_name(const char* e) {
   if (e && !std::strcmp(e, "w8r8")) return int(kCfgW8R8);
   if (e && !std::strcmp(e, "w8r16")) return int(kCfgW8R16);
   if (e && !std::strcmp(e, "w8r8acc")) return int(kCfgW8R8Acc);
+  if (e && !std::strcmp(e, "w8r4")) return int(kCfgW8R4);
   return int(kCfgAuto);
 }
 // ELSA_FWD_CFG (or elsa_dev_force_config) forces one of the d <= 64 configurations
@@ -209,6 +211,8 @@ CfgInfo cfg_info(int cfg) {
       return {128, 64, 1, 5.355, 4.1};
     case kCfgW8R8Acc:  // ~1% more per tile than w8r8 (profiles/round2_ab_acc.txt)
       return {128, 64, 1, 5.41, 4.1};
+    case kCfgW8R4:  // provisional (to be fitted)
+      return {64, 64, 1, 3.2, 3.0};
     // wide-head configurations: scaled from the w8r8 fit by GEMM length
     // (d + dv relative to 128), not fitted — the planner only compares kv
     // split counts within one of them
@@ -288,13 +292,25 @@ struct Plan {
   int splits;
   int64_t heads_per_batch;  // (b, h) pairs per launch batch when splits > 1
   bool cluster = false;     // splits merged inside one launch over DSMEM (no workspace, no K2)
+  int tail_s = 0;           // tail split: units >= tail_first run as tail_s key pieces
+  int64_t tail_first = 0;   // (final output, splits == 1; K2 merges the tail rows)
 };
+
+// Tail split (ELSA_TAIL: 0 off, 1 cost model (default), s >= 2 force s pieces):
+// when the units of a one-split plan leave the last wave partly empty, the
+// units of that wave run as s key pieces each (more, shorter CTAs) and a K2
+// merges their rows. Same launch, same kernel code for the full units.
+int g_tail_mode = [] {
+  const char* e = std::getenv("ELSA_TAIL");
+  return e ? std::atoi(e) : 1;
+}();
+bool tail_capable(int cfg) { return cfg == kCfgW4R8 || cfg == kCfgW8R8 || cfg == kCfgW8R8Acc; }
 
 // Cluster split merge (fwd_f32_kernel<..., CL = true>): the d, dv <= 64
 // configurations with 2..16 splits, final output only.
 constexpr int kMaxClusterSplits = 16;
 bool cluster_capable(int cfg, int64_t dv) {
-  return (cfg == kCfgW4R8 || cfg == kCfgW8R8) && dv <= 64;
+  return (cfg == kCfgW4R8 || cfg == kCfgW8R8 || cfg == kCfgW8R4) && dv <= 64;
 }
 
 double plan_cost(const CfgInfo& ci, int64_t ctas, int64_t tiles, int64_t rows, int64_t sms,
@@ -325,10 +341,11 @@ constexpr int kClusterAutoMaxSplits = 4;
 template <int W, int TK, int ST, int R>
 int max_active_clusters(int splits, DeviceCache* dc, int cfg_slot);
 
-int cluster_slot(int cfg) { return cfg == kCfgW8R8 ? 1 : 0; }
+int cluster_slot(int cfg) { return cfg == kCfgW8R8 ? 1 : (cfg == kCfgW8R4 ? 2 : 0); }
 
 int active_clusters(int cfg, int splits, DeviceCache* dc) {
   if (!dc || splits < 2 || splits > kMaxClusterSplits) return 0;
+  if (cfg == kCfgW8R4) return max_active_clusters<8, 64, 2, 4>(splits, dc, cluster_slot(cfg));
   return cfg == kCfgW8R8
              ? max_active_clusters<8, 64, ELSA_W8R8_STAGES, 8>(splits, dc, cluster_slot(cfg))
              : max_active_clusters<4, 64, ELSA_W4R8_STAGES, 8>(splits, dc, cluster_slot(cfg));
@@ -340,7 +357,10 @@ Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms,
   // head widths beyond 64 have one configuration each; d, dv <= 64 choose
   const int only = wide_cfg(sh->d, sh->dv);
   const bool wide = only >= 0;
-  const int first = wide ? only : 0, last = wide ? only + 1 : int(kCfgCount) + 1;
+  // d, dv <= 64 candidates: w4r8, w8r16, w8r8, the long-chain w8r8acc and the
+  // small-problem w8r4
+  static const int kNarrow[] = {kCfgW4R8, kCfgW8R16, kCfgW8R8, kCfgW8R8Acc, kCfgW8R4};
+  const int first = wide ? only : 0, last = wide ? only + 1 : int(sizeof(kNarrow) / sizeof(int));
   Plan best{first, 1, BH > 0 ? BH : 1};
   double best_t = 1e300;
   const int forced = wide ? int(kCfgAuto) : forced_cfg();
@@ -348,7 +368,8 @@ Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms,
   const int64_t head_bytes = sh->n_q * (2 + 64 * dv_slices(sh->dv)) * 4;  // one split of one (b, h) head
   for (int ci_ = first; ci_ < last; ++ci_) {
     // d, dv <= 64: w4r8, w8r16, w8r8, then the long-chain w8r8acc
-    const int cfg = (!wide && ci_ == int(kCfgCount)) ? int(kCfgW8R8Acc) : ci_;
+    const int cfg = wide ? ci_ : kNarrow[ci_];
+    if (cfg == kCfgW8R4 && forced != kCfgW8R4) continue;  // not auto-planned yet
     if (forced != kCfgAuto && cfg != forced) continue;
     const CfgInfo ci = cfg_info(cfg);
     const int64_t ctas = ceil_div(sh->n_q, ci.tq) * BH * slices;
@@ -406,6 +427,30 @@ Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms,
     const bool fits = maxc > 0 && nclu <= maxc && best.splits <= kClusterAutoMaxSplits;
     if (fits || (g_cluster_mode == 2 && maxc > 0)) {
       best.cluster = true;
+      best.heads_per_batch = BH;
+    }
+  }
+  if (allow_cluster && g_tail_mode != 0 && best.splits == 1 && !best.cluster &&
+      tail_capable(best.cfg) && sh->dv <= 64 && requested <= 0) {
+    const CfgInfo ci = cfg_info(best.cfg);
+    const int64_t U = ceil_div(sh->n_q, ci.tq) * BH;  // units (one CTA each)
+    const int64_t N = ceil_div(kv_len, ci.tk);       // key tiles per unit
+    const int64_t slots = int64_t(sms) * ci.ctas_per_sm;
+    const int64_t F = (U / slots) * slots, T = U - F;
+    // Measured rule (tools/time_tail.sh, profiles/round2_tail_split.txt): two
+    // pieces per tail unit pay only after >= 2 full waves with the last wave
+    // 50-75% full (BERT-base B8 H12 n512, w4r8: 151.5 -> 143.4 us); fuller or
+    // emptier last waves and more pieces measured equal or slower.
+    const double frac = double(T) / double(slots);
+    int bs = 0;
+    if (g_tail_mode >= 2)
+      bs = int(g_tail_mode < N ? g_tail_mode : N);
+    else if (F >= 2 * slots && frac >= 0.5 && frac < 0.75 && N >= 2)
+      bs = 2;
+    if (bs >= 2) bs = int(normalize_splits(bs, N));  // no empty pieces
+    if (bs >= 2 && T > 0 && F + T * bs < (int64_t(1) << 31)) {
+      best.tail_s = bs;
+      best.tail_first = F;
       best.heads_per_batch = BH;
     }
   }
@@ -533,7 +578,7 @@ int launch_fwd_cfg(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fwd)");
     dc->attr[slot] = true;
   }
-  const int64_t gx = int64_t(p.qtiles) * bh_count;
+  const int64_t gx = p.grid_units > 0 ? p.grid_units : int64_t(p.qtiles) * bh_count;
   if (gx >= (int64_t(1) << 31)) return ELSA_ERR_SHAPE;
   const dim3 grid{unsigned(gx), unsigned(splits), unsigned(ceil_div(s->dv, DV))};
   if constexpr (CL) {
@@ -606,6 +651,9 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
                cudaStream_t stream) {
   const int splits = plan.splits;
   if (plan.cluster) {
+    if (plan.cfg == kCfgW8R4)
+      return launch_fwd_cfg<8, 64, 2, 4, 64, 64, true>(p, s, q_st, k_st, v_st, splits, bh_count,
+                                                       kCfgW8R4, dc, stream);
     if (plan.cfg == kCfgW8R8)
       return launch_fwd_cfg<8, 64, ELSA_W8R8_STAGES, 8, 64, 64, true>(
           p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8, dc, stream);
@@ -622,6 +670,9 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
     case kCfgW8R8Acc:
       return launch_fwd_cfg<8, 64, ELSA_W8R8_STAGES, 8, 64, 64, false, true>(
           p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8Acc, dc, stream);
+    case kCfgW8R4:
+      return launch_fwd_cfg<8, 64, 2, 4>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R4, dc,
+                                         stream);
     case kCfgW8R8D128:
       return launch_fwd_cfg<8, 64, 2, 8, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
                                               kCfgW8R8D128, dc, stream);
@@ -732,7 +783,16 @@ void fill_common(FwdParams& p, const float* q, const float* k, const float* v,
   p.row_stride = 1;
 }
 
+int64_t tail_rows(const elsa_shape* s, const Plan& pl) {
+  const int tq = cfg_info(pl.cfg).tq;
+  const int64_t qt = ceil_div(s->n_q, tq);
+  const int64_t r0 = (pl.tail_first / qt) * s->n_q + (pl.tail_first % qt) * tq;
+  return s->B * s->H * s->n_q - r0;
+}
+
 size_t split_ws_bytes(const elsa_shape* s, const Plan& pl) {
+  if (pl.tail_s > 0)
+    return size_t(pl.tail_s) * size_t(tail_rows(s, pl)) * size_t(2 + 64) * sizeof(float) + 16;
   if (pl.splits <= 1 || pl.cluster) return 0;
   const size_t rows = size_t(pl.heads_per_batch) * size_t(s->n_q);
   // m | S | (pad to 16 bytes) | W
@@ -804,6 +864,53 @@ int run_forward(const float* q, const float* k, const float* v, const elsa_shape
     p.bh_begin = 0;
     p.mode = kModeFinal;
     return launch_fwd(p, shp, q_st, k_st, v_st, plan, BH, dc, strm);
+  }
+  if (plan.tail_s > 0 && final_out) {
+    // one forward launch: whole units, then the last wave's units as key
+    // pieces writing log2 partial states; K2 (PDL) merges the tail rows
+    const size_t need = split_ws_bytes(shp, plan);
+    if (!workspace || ws_bytes < need) return ELSA_ERR_WORKSPACE;
+    const int tq = cfg_info(plan.cfg).tq, tk = cfg_info(plan.cfg).tk;
+    const int64_t rows_t = tail_rows(shp, plan);
+    const int64_t ntiles = ceil_div(len, tk);
+    float* ws = static_cast<float*>(workspace);
+    p.bh_begin = 0;
+    p.mode = kModeFinal;
+    p.tail_first = int(plan.tail_first);
+    p.tail_splits = plan.tail_s;
+    p.tail_split_keys = int(ceil_div(ntiles, plan.tail_s) * tk);
+    p.tail_row0 = BH * shp->n_q - rows_t;
+    p.pm = ws;
+    p.pS = ws + int64_t(plan.tail_s) * rows_t;
+    p.pW = ws + ((int64_t(plan.tail_s) * rows_t * 2 + 3) & ~int64_t(3));
+    p.part_stride = rows_t;
+    p.pw_pitch = 64;
+    p.pw_vec = reinterpret_cast<uintptr_t>(p.pW) % 16 == 0;
+    p.grid_units = plan.tail_first +
+                   (ceil_div(shp->n_q, tq) * BH - plan.tail_first) * plan.tail_s;
+    if (int st = launch_fwd(p, shp, q_st, k_st, v_st, plan, BH, dc, strm)) return st;
+    MergeParams mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.m = p.pm;
+    mp.S = p.pS;
+    mp.W = p.pW;
+    mp.parts = plan.tail_s;
+    mp.rows = rows_t;
+    mp.dv = int(shp->dv);
+    mp.w_pitch = 64;
+    mp.part_stride = rows_t;
+    mp.log2_domain = 1;
+    mp.err = dc->err;
+    mp.finalize = 1;
+    mp.y = y;
+    mp.H = int(shp->H);
+    mp.n_q = int(shp->n_q);
+    mp.bh_begin = 0;
+    mp.row0 = p.tail_row0;
+    mp.ys_b = shp->y_stride[0];
+    mp.ys_h = shp->y_stride[1];
+    mp.ys_r = shp->y_stride[2];
+    return launch_merge(mp, strm, true);
   }
   if (plan.splits <= 1) {
     p.bh_begin = 0;
@@ -963,6 +1070,8 @@ HostLayout host_layout(const elsa_shape* s, int kv_splits, int sms, DeviceCache*
   HostLayout L;
   const int64_t BH = s->B * s->H;
   L.plan = plan_for(s, s->n_kv, kv_splits, sms, true, dc);
+  L.plan.tail_s = 0;  // groups re-plan nothing: the tail split is per whole problem
+  L.plan.tail_first = 0;
   const int64_t g = BH < kPipeMaxGroups ? (BH > 0 ? BH : 1) : kPipeMaxGroups;
   L.hpg = ceil_div(BH > 0 ? BH : 1, g);
   L.groups = int(ceil_div(BH > 0 ? BH : 1, L.hpg));
@@ -1052,6 +1161,9 @@ int elsa_dev_max_active_clusters(int cfg, int splits) {
 }
 
 void elsa_dev_set_cluster(int mode) { g_cluster_mode = mode < 0 ? 0 : (mode > 2 ? 2 : mode); }
+
+// Development aid: tail-split mode (0 off, 1 measured rule, s >= 2 force s pieces).
+void elsa_dev_set_tail(int mode) { g_tail_mode = mode < 0 ? 0 : mode; }
 
 // Development aid: force a d <= 64 configuration by name ("w4r8", "w8r8",
 // "w8r16", "w8r8acc"; anything else = the planner's choice).
@@ -1541,14 +1653,17 @@ int elsa_describe_plan(const elsa_shape* shp, int kv_splits, char* buf, size_t n
   static const char* names[] = {"w4r8",     "w8r16",        "w8r8",    "w8r8d128",
                                 "w8r8v128", "w8r8d128v128", "w8r8d96", "w8r8d96v128",
                                 "w8r8d256", "w4r8d256v128", "w8r8d32v32", "w8r8d96v96",
-                                "w8r8v96", "w8r8d128v96", "w4r8d256v256", "w8r8acc"};
-  static_assert(sizeof(names) / sizeof(names[0]) == kCfgW8R8Acc + 1, "one name per config");
-  if (pl.cfg < 0 || pl.cfg > kCfgW8R8Acc) return ELSA_ERR_SHAPE;
+                                "w8r8v96", "w8r8d128v96", "w4r8d256v256", "w8r8acc", "w8r4"};
+  static_assert(sizeof(names) / sizeof(names[0]) == kCfgW8R4 + 1, "one name per config");
+  if (pl.cfg < 0 || pl.cfg > kCfgW8R4) return ELSA_ERR_SHAPE;
   const CfgInfo ci = cfg_info(pl.cfg);
   const int64_t slices = ceil_div(shp->dv, cfg_dv(pl.cfg));
   const int64_t chain = ceil_div(ceil_div(shp->n_kv, ci.tk), pl.splits);
   std::string extra = slices > 1 ? " dv_slices=" + std::to_string(slices) : std::string();
   if (pl.cluster) extra += " cluster_merge=dsmem";
+  if (pl.tail_s > 0)
+    extra += " tail_split=" + std::to_string(pl.tail_s) + "x(units>=" +
+             std::to_string(pl.tail_first) + ")";
   if (chain > chain_cap(pl.cfg))
     extra += " chain_tiles=" + std::to_string(chain) + " (over the " +
              std::to_string(chain_cap(pl.cfg)) + "-tile cap: > kMaxSplits x cap keys)";

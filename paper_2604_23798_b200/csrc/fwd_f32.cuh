@@ -118,6 +118,13 @@ struct FwdParams {
   int pw_vec;           // float4 stores to pW legal
   int* err;
   unsigned long long* trace;  // ELSA_TRACE builds: per-warp phase timestamps
+  // Tail split (final-output plans whose last wave is partly empty): CTAs
+  // blockIdx.x >= tail_first are key pieces of the units from tail_first on,
+  // tail_splits per unit of tail_split_keys keys each, writing log2 partial
+  // states at workspace row (row - tail_row0) for a K2 merge of those rows.
+  int tail_first, tail_splits, tail_split_keys;
+  int64_t tail_row0;
+  int64_t grid_units;  // grid x when != 0 (tail-split launches)
   int q_vec, k_vec, v_vec;    // copy engine: 16-byte aligned rows (base and strides)
 };
 
@@ -387,16 +394,24 @@ __device__ __forceinline__ void cluster_merge_epilogue(const FwdParams& p, float
   // every consumer warp is done reading the ring (its last GEMM2) before any
   // warp overwrites it with states
   asm volatile("bar.sync 1, %0;" ::"r"(T::W * 32) : "memory");
+  float lrow[R];  // row normalizers, all rows' butterflies interleaved (same order per row)
+#pragma unroll
+  for (int ip = 0; ip < RP; ++ip) {
+    lrow[2 * ip] = ptx::lo2(l2[ip]);
+    lrow[2 * ip + 1] = ptx::hi2(l2[ip]);
+  }
+#pragma unroll
+  for (int sh = 1; sh <= 16; sh <<= 1) {
+    if (sh == 8) continue;  // lane bit 3 is the row group
+#pragma unroll
+    for (int i = 0; i < R; ++i) lrow[i] += __shfl_xor_sync(0xffffffffu, lrow[i], sh);
+  }
 #pragma unroll
   for (int ip = 0; ip < RP; ++ip) {
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       const int i = 2 * ip + half;
-      float l = half ? ptx::hi2(l2[ip]) : ptx::lo2(l2[ip]);
-      l += __shfl_xor_sync(0xffffffffu, l, 1);
-      l += __shfl_xor_sync(0xffffffffu, l, 2);
-      l += __shfl_xor_sync(0xffffffffu, l, 4);
-      l += __shfl_xor_sync(0xffffffffu, l, 16);
+      const float l = lrow[i];
       const int lr = warp * WR + rg + 2 * i;
       float4 w;
       w.x = half ? ptx::hi2(o2[ip][0]) : ptx::lo2(o2[ip][0]);
@@ -410,7 +425,6 @@ __device__ __forceinline__ void cluster_merge_epilogue(const FwdParams& p, float
       }
     }
   }
-  (void)R;
   cg::cluster_group cluster = cg::this_cluster();
   cluster.sync();  // release our states / acquire the peers'
   const int parts = int(cluster.num_blocks());
@@ -471,18 +485,26 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  const int qtile = blockIdx.x % p.qtiles;
-  const int bh_rel = blockIdx.x / p.qtiles;
+  // (selects, not a branch: every value stays warp-uniform)
+  const int bx = int(blockIdx.x);
+  const bool tail = p.tail_splits > 0 && bx >= p.tail_first;
+  const int tsp = tail ? p.tail_splits : 1;
+  const int tj = (tail ? bx - p.tail_first : 0) / tsp;
+  const int unit = tail ? p.tail_first + tj : bx;
+  const int split = tail ? bx - p.tail_first - tj * tsp : int(blockIdx.y);
+  const int split_keys = tail ? p.tail_split_keys : p.split_keys;
+  const int mode = tail ? int(kModePartialLog2) : p.mode;
+  const int qtile = unit % p.qtiles;
+  const int bh_rel = unit / p.qtiles;
   const int bh = bh_rel + p.bh_begin;
-  const int split = blockIdx.y;
   const int b = bh / p.H;
   const int h = bh - b * p.H;
   const int q0 = qtile * T::TQ;
   const int col0 = int(blockIdx.z) * T::DV;  // this CTA's column slice of V / W / Y
 
-  const int64_t lo64 = int64_t(p.kv_begin) + int64_t(split) * p.split_keys;
+  const int64_t lo64 = int64_t(p.kv_begin) + int64_t(split) * split_keys;
   const int split_lo = int(lo64 < p.kv_end ? lo64 : p.kv_end);
-  const int kv_hi = int(lo64 + p.split_keys < p.kv_end ? lo64 + p.split_keys : p.kv_end);
+  const int kv_hi = int(lo64 + split_keys < p.kv_end ? lo64 + split_keys : p.kv_end);
   const int ntiles = kv_hi > split_lo ? (kv_hi - split_lo + TK - 1) / TK : 0;
 
   trace_cta(p, 0);
@@ -862,22 +884,33 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   }
 
   // ---------------- epilogue ----------------
+  // row normalizers: the butterfly over the 16 key-group lanes for all R rows
+  // at once (independent shuffles overlap; the per-row order of additions is
+  // unchanged)
+  float lrow[R];
+#pragma unroll
+  for (int ip = 0; ip < RP; ++ip) {
+    lrow[2 * ip] = ptx::lo2(l2[ip]);
+    lrow[2 * ip + 1] = ptx::hi2(l2[ip]);
+  }
+#pragma unroll
+  for (int sh = 1; sh <= 16; sh <<= 1) {
+    if (sh == 8) continue;  // lane bit 3 is the row group
+#pragma unroll
+    for (int i = 0; i < R; ++i) lrow[i] += __shfl_xor_sync(0xffffffffu, lrow[i], sh);
+  }
 #pragma unroll
   for (int ip = 0; ip < RP; ++ip) {
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       const int i = 2 * ip + half;
-      float l = half ? ptx::hi2(l2[ip]) : ptx::lo2(l2[ip]);
-      l += __shfl_xor_sync(0xffffffffu, l, 1);
-      l += __shfl_xor_sync(0xffffffffu, l, 2);
-      l += __shfl_xor_sync(0xffffffffu, l, 4);
-      l += __shfl_xor_sync(0xffffffffu, l, 16);
+      const float l = lrow[i];
       float o[CV];
 #pragma unroll
       for (int c = 0; c < CV; ++c) o[c] = half ? ptx::hi2(o2[ip][c]) : ptx::lo2(o2[ip][c]);
       const int qrow = q0 + warp * WR + rg + 2 * i;
       if (qrow >= p.n_q) continue;
-      if (p.mode == kModeFinal) {
+      if (mode == kModeFinal) {
         // engine.py:377-378: the normalizer must be finite and positive
         if (!(l > 0.f) || !isfinite(l)) {
           if (g == 0) atomicCAS(p.err, 0, 3);
@@ -919,9 +952,10 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
         }
       } else {
         const int64_t row = int64_t(bh_rel) * p.n_q + qrow;  // relative to this batch
-        const int64_t idx = int64_t(split) * p.part_stride + row * p.row_stride;
+        const int64_t idx =
+            int64_t(split) * p.part_stride + (tail ? row - p.tail_row0 : row) * p.row_stride;
         if (g == 0 && col0 == 0) {  // m and S are the same in every column slice
-          const float m = (p.mode == kModePartialNat) ? mrow[i] * 0.69314718055994531f : mrow[i];
+          const float m = (mode == kModePartialNat) ? mrow[i] * 0.69314718055994531f : mrow[i];
           p.pm[idx] = m;
           p.pS[idx] = l;
         }

@@ -38,7 +38,8 @@ struct MergeParams {
   // finalize output: row -> (b,h,q) via n_q and H, strided Y
   float* y;
   int H, n_q;
-  int bh_begin;  // finalize: row r maps to flattened (b, h) = r / n_q + bh_begin
+  int bh_begin;  // finalize: row r maps to flattened (b, h) = (r + row0) / n_q + bh_begin
+  int64_t row0;  // finalize: output row of workspace row 0 (tail-split merges)
   int64_t ys_b, ys_h, ys_r;
   // non-finalize output (dense [rows][out_pitch])
   float* m_out;
@@ -127,8 +128,9 @@ __global__ void __launch_bounds__(256) merge_f32_kernel(const MergeParams p) {
     }
     float* yrow;
     if (p.n_q > 0) {
-      const int64_t bh_rel = row / p.n_q;
-      const int64_t q = row - bh_rel * p.n_q;
+      const int64_t orow = row + p.row0;
+      const int64_t bh_rel = orow / p.n_q;
+      const int64_t q = orow - bh_rel * p.n_q;
       const int64_t bh = bh_rel + p.bh_begin;
       const int64_t b = bh / p.H, h = bh - b * p.H;
       yrow = p.y + b * p.ys_b + h * p.ys_h + q * p.ys_r;

@@ -83,3 +83,36 @@ def test_cluster_strided_output_and_negative_scale(cluster_mode):
     cluster_mode(0)
     ref = elsa.scaled_dot_product_attention(q, k, v, kv_splits=4, scale=-0.3)
     assert torch.equal(out, ref)
+
+
+# ---- tail split (last wave's units as key pieces + K2 over their rows) ----
+
+@pytest.mark.parametrize("shape,mode", [((8, 12, 512), 1), ((8, 12, 512), 3), ((8, 16, 512), 2),
+                                        ((16, 12, 500), 5)])
+def test_tail_split_parity_and_full_units_bitwise(shape, mode):
+    """Tail-split plans (ELSA_TAIL / set_tail_mode): every row within the
+    reference bound vs FP64, and the rows of the whole units (before the
+    tail) bitwise equal to the plan without the tail split (same kernel code
+    for them)."""
+    b, h, n = shape
+    rng = np.random.default_rng(b * 1000 + n)
+    Q, K, V = (rng.standard_normal((b, h, n, 64)).astype(np.float32) for _ in range(3))
+    q, k, v = (torch.from_numpy(x).to(DEV) for x in (Q, K, V))
+    try:
+        elsa.attention.set_tail_mode(0)
+        y0 = elsa.scaled_dot_product_attention(q, k, v)
+        elsa.attention.set_tail_mode(mode)
+        plan = elsa.describe_plan(q, k, v)
+        y1 = elsa.scaled_dot_product_attention(q, k, v, check_numerics=True)
+    finally:
+        elsa.attention.set_tail_mode(1)
+    assert "tail_split=" in plan, plan
+    first = int(plan.split("units>=")[1].rstrip(")"))
+    tq = int(plan.split("tq=")[1].split()[0])
+    qt = -(-n // tq)
+    row0 = (first // qt) * n + (first % qt) * tq
+    f0, f1 = y0.reshape(-1, 64), y1.reshape(-1, 64)
+    assert torch.equal(f0[:row0], f1[:row0])
+    ref = oracle.naive_attention(Q.astype(np.float64), K.astype(np.float64), V.astype(np.float64))
+    err = oracle.row_rel_err(y1.cpu().numpy(), ref)
+    assert err.max() <= oracle.bound_threshold(n), err.max()
