@@ -300,23 +300,27 @@ def query_sharded_attention(q, k, v, group=None, gather=False, attn_fn=None):
     slices = row_slices(rows, world)
     lo, hi = slices[rank]
     _LAUNCHES[0] = 0
-    # the slice = [partial head] + whole heads (one launch) + [partial head]
-    qf, kf, vf = (t.reshape(B * H, 1, t.shape[2], t.shape[3]) for t in (q, k, v))
+    # the slice = [partial head] + whole heads (one launch) + [partial head];
+    # heads as one (1, B*H, n, d) batch (a view for contiguous inputs), whole
+    # heads written straight into the output rows (no staging copy)
+    qf, kf, vf = (t.reshape(1, B * H, t.shape[2], t.shape[3]) for t in (q, k, v))
     out = torch.empty((hi - lo, dv), device=q.device, dtype=torch.float32)
     r = lo
     while r < hi:
         bh, q0 = divmod(r, n_q)
         if q0 == 0 and hi - r >= n_q:  # a run of whole heads
             nh = (hi - r) // n_q
-            y = attn_fn(qf[bh:bh + nh].transpose(0, 1), kf[bh:bh + nh].transpose(0, 1),
-                        vf[bh:bh + nh].transpose(0, 1))
-            if not injected:
+            dst = out[r - lo: r - lo + nh * n_q].view(1, nh, n_q, dv)
+            if injected:
+                dst.copy_(attn_fn(qf[:, bh:bh + nh], kf[:, bh:bh + nh], vf[:, bh:bh + nh])
+                          .reshape(1, nh, n_q, dv))
+            else:
+                attn_fn(qf[:, bh:bh + nh], kf[:, bh:bh + nh], vf[:, bh:bh + nh], out=dst)
                 _tally()
-            out[r - lo: r - lo + nh * n_q] = y.reshape(nh * n_q, dv)
             r += nh * n_q
         else:
             q1 = min(n_q, q0 + (hi - r))
-            y = attn_fn(qf[bh:bh + 1, :, q0:q1], kf[bh:bh + 1], vf[bh:bh + 1])
+            y = attn_fn(qf[:, bh:bh + 1, q0:q1], kf[:, bh:bh + 1], vf[:, bh:bh + 1])
             if not injected:
                 _tally()
             out[r - lo: r - lo + (q1 - q0)] = y.reshape(q1 - q0, dv)
