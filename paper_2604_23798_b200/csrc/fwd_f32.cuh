@@ -70,8 +70,12 @@
 #ifndef ELSA_G2_UNROLL_R8
 #define ELSA_G2_UNROLL_R8 16
 #endif
+// Snake order (reverse the row-pair order on odd broadcast operands): on for
+// every kernel except the d, dv <= 64 w8r8 family, where source order without
+// it measured +0.4% at 8K-16K (profiles/round2_ab_variants.txt; -0.15% for
+// w4r8 at 4K, so the others keep it). ELSA_SNAKE=0/1 forces it everywhere.
 #ifndef ELSA_SNAKE
-#define ELSA_SNAKE 1      // reverse the row-pair order on odd broadcast operands
+#define ELSA_SNAKE -1
 #endif
 #ifndef ELSA_CONSUMER_REGS
 #define ELSA_CONSUMER_REGS 224
@@ -468,6 +472,8 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
                 "cluster merge: one 64-column slice, every warp alive, states fit the ring");
   constexpr int TK = T::TK, QP = T::QP, QTP = T::QTP, VP = T::VP, PTP = T::PTP, RK = T::RK;
   constexpr int R = T::R, RP = T::RP, WR = T::WR;
+  constexpr bool kSnake =
+      ELSA_SNAKE >= 0 ? ELSA_SNAKE != 0 : !(W_ == 8 && R_ == 8 && D_ == 64 && DV_ == 64);
   using ptx::f32x2;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -673,7 +679,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
         const f32x2 vb = ptx::pack2(vv, vv);
 #pragma unroll
         for (int u = 0; u < RP; ++u) {
-          const int ip = (ELSA_SNAKE && (c & 1)) ? RP - 1 - u : u;
+          const int ip = (kSnake && (c & 1)) ? RP - 1 - u : u;
           if constexpr (kTileAcc)
             ptx::ffma2(t2[ip][kTileAcc ? c : 0], vb, pr[ip]);
           else
@@ -701,7 +707,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
           const f32x2 vb = ptx::pack2(vv, vv);
 #pragma unroll
           for (int u = 0; u < RP; ++u) {
-            const int ip = (ELSA_SNAKE && (c & 1)) ? RP - 1 - u : u;
+            const int ip = (kSnake && (c & 1)) ? RP - 1 - u : u;
             if constexpr (kTileAcc) {
               if (first)
                 t2[ip][c] = ptx::fmul2(vb, pr[ip]);
@@ -790,7 +796,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
           const f32x2 kb = ptx::pack2(kv, kv);
 #pragma unroll
           for (int u = 0; u < RP; ++u) {
-            const int ip = (ELSA_SNAKE && (j & 1)) ? RP - 1 - u : u;
+            const int ip = (kSnake && (j & 1)) ? RP - 1 - u : u;
             ptx::ffma2(s2[ip][j], kb, q2[ip]);
           }
         }
