@@ -80,7 +80,8 @@ int elsa_resolve_kv_splits(const elsa_shape* shp, int requested);
 
 /* Workspace bytes elsa_fwd_f32 needs for `kv_splits` (0 = auto). Zero when
  * the resolved split count is 1 or the splits merge inside the launch
- * (thread-block-cluster merge over distributed shared memory). */
+ * (thread-block-cluster merge over distributed shared memory); non-zero for
+ * an auto plan whose last partly-empty wave runs as key pieces (tail split). */
 size_t elsa_workspace_bytes(const elsa_shape* shp, int kv_splits);
 
 /* Workspace bytes elsa_partial_f32 needs for keys [kv_begin, kv_end) and
