@@ -235,7 +235,10 @@ struct FwdTraits {
   // Phase-offsetting the two warps of each SMSP (see `lagged` in the kernel)
   // measured no gain on B200 (per-warp phase trace) and costs registers, so
   // it is compiled out.
-  static constexpr bool kLag = false;
+#ifndef ELSA_LAG
+#define ELSA_LAG 0
+#endif
+  static constexpr bool kLag = ELSA_LAG != 0 && W >= 8 && !kHalfP;
   static constexpr int CONSUMER_REGS = ELSA_CONSUMER_REGS;  // after setmaxnreg.inc (R = 16 only)
   static_assert(!kRegSplit || (W % 4 == 0), "register split needs whole consumer warpgroups");
   static_assert(!kRegSplit || PRODUCER_REGS + (W / 4) * CONSUMER_REGS <= 512,
@@ -628,7 +631,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   f32x2 l2[RP];     // running normalizer partials (this lane's keys)
   // ELSA_TILE_ACC: this tile's P V (t2) and the running side's factor (corr_t)
   constexpr bool kTileAcc = ACC && CV <= 8;  // V slices of <= 128 columns
-  static_assert(!(kTileAcc && T::kLag), "per-tile accumulation assumes the in-order GEMM2");
+  constexpr bool kLagK = T::kLag && !kTileAcc;  // per-tile accumulation assumes the in-order GEMM2
   f32x2 t2[RP][kTileAcc ? CV : 1];
   f32x2 corr_t[RP];
 #pragma unroll
@@ -762,7 +765,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   // w and w + 4, W >= 8): the upper half runs GEMM2 of the previous tile
   // before GEMM1 of the current one, so its latency-bound softmax section
   // overlaps the partner's FFMA2 stream instead of coinciding with it.
-  const bool lagged = T::kLag && warp >= T::W / 2;
+  const bool lagged = kLagK && warp >= T::W / 2;
 
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % T::STAGES;
@@ -861,7 +864,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
     }
     if constexpr (T::kHalfP) {
       // first key half through the (half-size) P area, then the second half
-      static_assert(!T::kLag, "halved P assumes the in-order GEMM2");
+      static_assert(!kLagK, "halved P assumes the in-order GEMM2");
       store_p(s2, 0, RK / 2);
       __syncwarp();
       gemm2(t, 0);
