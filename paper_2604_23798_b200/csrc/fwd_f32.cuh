@@ -893,6 +893,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
   }
 
   // ---------------- epilogue ----------------
+  trace_mark(p, warp, ntiles, 0);
   // row normalizers: the butterfly over the 16 key-group lanes for all R rows
   // at once (independent shuffles overlap; the per-row order of additions is
   // unchanged)
@@ -907,6 +908,82 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
     if (sh == 8) continue;  // lane bit 3 is the row group
 #pragma unroll
     for (int i = 0; i < R; ++i) lrow[i] += __shfl_xor_sync(0xffffffffu, lrow[i], sh);
+  }
+  trace_mark(p, warp, ntiles, 1);
+  if constexpr (T::DV == 64 && T::W <= 4 && (TK / T::PH) * PTP >= WR * 66) {
+    // Staged epilogue (64-column slices): the warp parks its rows' W, S and
+    // anchor in its own P area, then one compact loop writes each row as 16
+    // coalesced float4 chunks (Y = W / S with the same IEEE division, or the
+    // partial state). A fully unrolled per-lane epilogue was ~25 KB of code
+    // run once per CTA. Measured (profiles/round2_ab_epilogue.txt): BERT-base
+    // 145.4 -> 141.3 us, H16 4K +0.8%; the w8r8 kernels keep the unrolled
+    // form (their main loop's schedule moved with it: 16K -0.5%).
+    float* stg = pw;  // [WR][64] W | S[WR] | m[WR]
+    float* sl = stg + WR * 64;
+    float* sm = sl + WR;
+#pragma unroll
+    for (int ip = 0; ip < RP; ++ip) {
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int i = 2 * ip + half, r = rg + 2 * i;
+        const float4 w = half ? make_float4(ptx::hi2(o2[ip][0]), ptx::hi2(o2[ip][1]),
+                                            ptx::hi2(o2[ip][2]), ptx::hi2(o2[ip][3]))
+                              : make_float4(ptx::lo2(o2[ip][0]), ptx::lo2(o2[ip][1]),
+                                            ptx::lo2(o2[ip][2]), ptx::lo2(o2[ip][3]));
+        *reinterpret_cast<float4*>(stg + r * 64 + 4 * g) = w;
+        if (g == 0) {
+          sl[r] = lrow[i];
+          sm[r] = mrow[i];
+        }
+      }
+    }
+    __syncwarp();
+    const int qw = q0 + warp * WR;
+    const int rows_here = p.n_q - qw < WR ? p.n_q - qw : WR;
+#pragma unroll 1
+    for (int idx = lane; idx < rows_here * 16; idx += 32) {
+      const int r = idx >> 4, c4 = idx & 15;
+      const int qrow = qw + r;
+      const float4 w = *reinterpret_cast<const float4*>(stg + r * 64 + 4 * c4);
+      const float l = sl[r];
+      const int col = col0 + 4 * c4;
+      if (mode == kModeFinal) {
+        // engine.py:377-378: the normalizer must be finite and positive
+        if (c4 == 0 && (!(l > 0.f) || !isfinite(l))) atomicCAS(p.err, 0, 3);
+        const float4 y = make_float4(__fdiv_rn(w.x, l), __fdiv_rn(w.y, l), __fdiv_rn(w.z, l),
+                                     __fdiv_rn(w.w, l));
+        float* yrow = p.y + int64_t(b) * p.ys_b + int64_t(h) * p.ys_h + int64_t(qrow) * p.ys_r;
+        if (p.y_vec && col + 3 < p.dv) {
+          *reinterpret_cast<float4*>(yrow + col) = y;
+        } else {
+          if (col < p.dv) yrow[col] = y.x;
+          if (col + 1 < p.dv) yrow[col + 1] = y.y;
+          if (col + 2 < p.dv) yrow[col + 2] = y.z;
+          if (col + 3 < p.dv) yrow[col + 3] = y.w;
+        }
+      } else {
+        const int64_t row = int64_t(bh_rel) * p.n_q + qrow;  // relative to this batch
+        const int64_t sidx =
+            int64_t(split) * p.part_stride + (tail ? row - p.tail_row0 : row) * p.row_stride;
+        if (c4 == 0 && col0 == 0) {  // m and S are the same in every column slice
+          const float m = (mode == kModePartialNat) ? sm[r] * 0.69314718055994531f : sm[r];
+          p.pm[sidx] = m;
+          p.pS[sidx] = l;
+        }
+        float* wrow = p.pW + sidx * p.pw_pitch;
+        if (p.pw_vec && col + 3 < p.dv) {
+          *reinterpret_cast<float4*>(wrow + col) = w;
+        } else {
+          if (col < p.dv) wrow[col] = w.x;
+          if (col + 1 < p.dv) wrow[col + 1] = w.y;
+          if (col + 2 < p.dv) wrow[col + 2] = w.z;
+          if (col + 3 < p.dv) wrow[col + 3] = w.w;
+        }
+      }
+    }
+    trace_mark(p, warp, ntiles, 2);
+    trace_cta(p, 1);
+    return;
   }
 #pragma unroll
   for (int ip = 0; ip < RP; ++ip) {
@@ -1003,6 +1080,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
       }
     }
   }
+  trace_mark(p, warp, ntiles, 2);
   trace_cta(p, 1);
 }
 

@@ -46,3 +46,7 @@ for c in range(min(4, ncta)):
     print(f"CTA{c} (SM {a[c,2]}): first tile mark +{first} ns, last tile end +{last} ns, CTA end +{a[c,1]-s0} ns, "
           f"tiles/warp {int((w[0, :, 0] > 0).sum())}, mean tile {np.mean(w[:, :, 4][w[:, :, 4] > 0] - w[:, :, 0][w[:, :, 4] > 0]):.0f} ns")
     print("   per-tile total (warp0):", (w[0, :, 4] - w[0, :, 0])[:16].tolist())
+    nt = int((w[0, :, 4] > 0).sum())
+    if nt < w.shape[1]:
+        e = w[:, nt, :3] - s0
+        print("   epilogue marks (start, after normalizers, end) per warp:", e.tolist())
