@@ -43,7 +43,7 @@ constexpr int kMaxDevices = 64;
 #ifndef ELSA_W4R8_STAGES
 #define ELSA_W4R8_STAGES 2
 #endif
-constexpr int kAttrSlots = 42;
+constexpr int kAttrSlots = 46;
 constexpr int kMaxSplits = kMergeMaxParts;
 constexpr double kLog2e = 1.4426950408889634074;
 
@@ -801,13 +801,13 @@ size_t split_ws_bytes(const elsa_shape* s, const Plan& pl) {
 
 bool encode_map16(CUtensorMap* map, const void* base, int64_t inner, int64_t rows, int64_t H,
                   int64_t B,
-                  const int64_t st[3], bool bf16) {
+                  const int64_t st[3], bool bf16, int box_rows = 128) {
   auto enc = encoder();
   if (!enc) return false;
   // inner < 64: the 64-wide box is zero-filled past the row (OOB fill)
   cuuint64_t dims[4] = {cuuint64_t(inner), cuuint64_t(rows), cuuint64_t(H), cuuint64_t(B)};
   cuuint64_t strides[3] = {cuuint64_t(st[2] * 2), cuuint64_t(st[1] * 2), cuuint64_t(st[0] * 2)};
-  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t box[4] = {64, cuuint32_t(box_rows), 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
                    const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1306,10 +1306,19 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
   for (int i = 0; i < 3; ++i)
     if (y_st[i] < 0) return ELSA_ERR_SHAPE;
   const bool bf16 = is_bf16 != 0;
+  // 64 < d <= 128: 128-key tiles with P aliased over S. ELSA_TC_TK=64 selects
+  // the 64-key-tile kernel (no aliasing, S_g(t+1) overlaps the exponentials):
+  // measured slower (BF16 16K 975 vs 1224, 64K 922 vs 1096; faster only at
+  // n = 1K, 409 vs 350 TFLOP/s; profiles/round2_tc_d128_tk64.txt)
+  static const int tc_tk = [] {
+    const char* e = std::getenv("ELSA_TC_TK");
+    return e && std::atoi(e) == 64 ? 64 : 128;
+  }();
+  const int kv_box = wide16 ? tc_tk : 128;
   CUtensorMap maps[3];
   if (!encode_map16(&maps[0], q, shp->d, shp->n_q, shp->H, shp->B, q_st, bf16) ||
-      !encode_map16(&maps[1], k, shp->d, shp->n_kv, shp->H, shp->B, k_st, bf16) ||
-      !encode_map16(&maps[2], v, shp->dv, shp->n_kv, shp->H, shp->B, v_st, bf16))
+      !encode_map16(&maps[1], k, shp->d, shp->n_kv, shp->H, shp->B, k_st, bf16, kv_box) ||
+      !encode_map16(&maps[2], v, shp->dv, shp->n_kv, shp->H, shp->B, v_st, bf16, kv_box))
     return ELSA_ERR_SHAPE;
   TcParams p;
   std::memset(&p, 0, sizeof(p));
@@ -1357,9 +1366,15 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
         p, maps[0], maps[1], maps[2]);
     return ELSA_OK;
   };
-  const int base = kAttrSlots - 8;  // the last eight slots
+  const int base = kAttrSlots - 12;  // the last twelve slots
   int st;
-  if (wide16 && groups == 2)
+  if (wide16 && tc_tk == 64 && groups == 2)
+    st = bf16 ? launch(TcTraits<2, 128, 64>{}, fwd_tc_kernel<true, 2, 128, 64>, base + 11)
+              : launch(TcTraits<2, 128, 64>{}, fwd_tc_kernel<false, 2, 128, 64>, base + 10);
+  else if (wide16 && tc_tk == 64)
+    st = bf16 ? launch(TcTraits<1, 128, 64>{}, fwd_tc_kernel<true, 1, 128, 64>, base + 9)
+              : launch(TcTraits<1, 128, 64>{}, fwd_tc_kernel<false, 1, 128, 64>, base + 8);
+  else if (wide16 && groups == 2)
     st = bf16 ? launch(TcTraits<2, 128>{}, fwd_tc_kernel<true, 2, 128>, base + 7)
               : launch(TcTraits<2, 128>{}, fwd_tc_kernel<false, 2, 128>, base + 6);
   else if (wide16)

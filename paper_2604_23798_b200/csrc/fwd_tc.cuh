@@ -156,12 +156,19 @@ constexpr float kRescaleLog2 = 8.f;
 // swizzle-atom blocks). At D = 128, P is written over its own tile's S in
 // TMEM (kAliasP) so that two query tiles (S/P 128 + W 128 columns each) fit
 // the 512 columns; S_g(t+1) is then issued only after P_g(t) V.
-template <int GROUPS, int D_ = 64>
+//
+// TK_ = 64 (D = 128 only): 64-key tiles. S (64 columns), P (32) and W (128)
+// of both groups fit the 512 TMEM columns without aliasing, so S_g(t+1) is
+// issued as soon as S_g(t) is in registers (overlapping the exponentials) as
+// at D = 64, instead of after P_g(t) V.
+template <int GROUPS, int D_ = 64, int TK_ = 128>
 struct TcTraits {
-  static constexpr int TQ = 128, TK = 128, D = D_;
+  static constexpr int TQ = 128, TK = TK_, D = D_;
   static_assert(D == 64 || D == 128, "head width");
-  static constexpr bool kAliasP = D == 128;
-  static constexpr int STAGES = D == 64 ? ELSA_TC_STAGES : 2;  // 2 x 64 KB stages at D = 128
+  static_assert(TK == 128 || (TK == 64 && D == 128), "key tile");
+  static constexpr bool kAliasP = D == 128 && TK == 128;
+  // stages: D = 64 ELSA_TC_STAGES x 32 KB; D = 128: 2 x 64 KB, or 4 x 32 KB with 64-key tiles
+  static constexpr int STAGES = D == 64 ? ELSA_TC_STAGES : (TK == 64 ? 4 : 2);
   static constexpr int DB = D / 64;                          // 128-byte column blocks per row
   static constexpr int ROWS = GROUPS * TQ;                   // query rows per CTA
   static constexpr int Q_BLOCK = TQ * 128, K_BLOCK = TK * 128, V_BLOCK = TK * 128;
@@ -192,12 +199,12 @@ struct TcTraits {
   static constexpr int THREADS = kRegSplit ? (SOFTMAX_WARPS + 4) * 32 : (SOFTMAX_WARPS + 2) * 32;
   static constexpr int SOFTMAX_REGS = 232, OTHER_REGS = 40;
   static_assert(!kRegSplit || 2 * (SOFTMAX_REGS - 168) <= 168 - OTHER_REGS, "setmaxnreg budget");
-  static constexpr uint32_t S_COL = 0;             // group g: S at 128 g
-  static constexpr uint32_t O_COL = 128 * GROUPS;  // group g: W (P V accumulator) at O_COL + D g
+  static constexpr uint32_t S_COL = 0;             // group g: S at TK g
+  static constexpr uint32_t O_COL = TK * GROUPS;   // group g: W (P V accumulator) at O_COL + D g
   // group g: P (16-bit, two per 32-bit column) at P_COL + P_STRIDE g — the A
   // operand of P V read straight from TMEM (no shared-memory round trip)
-  static constexpr uint32_t P_COL = kAliasP ? S_COL : (128 + D) * GROUPS;
-  static constexpr uint32_t P_STRIDE = kAliasP ? 128 : 64;
+  static constexpr uint32_t P_COL = kAliasP ? S_COL : (TK + D) * GROUPS;
+  static constexpr uint32_t P_STRIDE = kAliasP ? 128 : TK / 2;
   static constexpr uint32_t TMEM_NEED = (O_COL + D * GROUPS > P_COL + P_STRIDE * GROUPS)
                                              ? O_COL + D * GROUPS
                                              : P_COL + P_STRIDE * GROUPS;
@@ -206,12 +213,12 @@ struct TcTraits {
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
-template <bool kBF16, int GROUPS, int D_ = 64>
-__global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
+template <bool kBF16, int GROUPS, int D_ = 64, int TK_ = 128>
+__global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
                   const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV) {
-  using T = TcTraits<GROUPS, D_>;
+  using T = TcTraits<GROUPS, D_, TK_>;
   extern __shared__ unsigned char smem_dyn[];
   // 1024-byte alignment for the 128B-swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
   const uint32_t tmem = *tmem_base_slot;
 
   constexpr int kFmt = kBF16 ? 1 : 0;
-  constexpr uint32_t kIdescS = tc::instr_desc_f16(kFmt, false, false, 128, 128);
+  constexpr uint32_t kIdescS = tc::instr_desc_f16(kFmt, false, false, 128, T::TK);
   constexpr uint32_t kIdescO = tc::instr_desc_f16(kFmt, false, true, 128, 64);
 
   // MMA issue for group g (warp-uniform; the elected `leader` lane issues)
@@ -267,7 +274,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
     const int s = t % T::STAGES;
     const uint32_t q_addr = ptx::smem_u32(smem + T::OFF_Q + g * T::Q_BYTES);
     const uint32_t k_addr = ptx::smem_u32(smem + T::OFF_K + s * T::K_BYTES);
-    const uint32_t d = tmem + T::S_COL + g * 128;
+    const uint32_t d = tmem + T::S_COL + g * T::TK;
 #pragma unroll
     for (int kk = 0; kk < T::D / 16; ++kk) {  // K-steps of 16 elements = 32 B
       const uint32_t blk = kk >> 2, off = (kk & 3) * 32;  // 64-element column block
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
     const int g = warp >> 2;
     const int row = (warp & 3) * 32 + lane;
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-    const uint32_t s_tm = tmem + lane_base + T::S_COL + g * 128;
+    const uint32_t s_tm = tmem + lane_base + T::S_COL + g * T::TK;
     const uint32_t o_tm = tmem + lane_base + T::O_COL + g * T::D;
     const float c2 = p.c;
     const float cs = p.neg ? -c2 : c2;  // exponent = s_raw * cs - m
@@ -417,9 +424,10 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
       ptx::mbar_wait(&s_full[g], t & 1);
       if (lane == 0) TC_MARK(warp, t, 1);
       tc::fence_after_sync();
-      float s[128];
+      constexpr int TK = T::TK;
+      float s[TK];
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
+      for (int ch = 0; ch < TK / 32; ++ch) {
         uint32_t r[32];
         tc::tmem_ld_32x32b_x32(s_tm + ch * 32, r);
 #pragma unroll
@@ -442,7 +450,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
       const int kv_hi = p.n_kv - t * T::TK;  // valid keys in this tile
       if (kv_hi < T::TK) {                   // tail tile (warp-uniform): mask past n_kv
 #pragma unroll
-        for (int i = 0; i < 128; ++i)
+        for (int i = 0; i < TK; ++i)
           if (i >= kv_hi) s[i] = p.neg ? CUDART_INF_F : -CUDART_INF_F;
       }
       // row max of the signed scores, in log2 units (warp-uniform sign branch;
@@ -454,14 +462,14 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[j] = s[j];
 #pragma unroll
-          for (int i = 8; i < 128; i += 8)
+          for (int i = 8; i < TK; i += 8)
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = fmaxf(acc[j], s[i + j]);
         } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) acc[j] = -s[j];
 #pragma unroll
-          for (int i = 8; i < 128; i += 8)
+          for (int i = 8; i < TK; i += 8)
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[j] = fmaxf(acc[j], -s[i + j]);
         }
@@ -504,8 +512,9 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
       ptx::f32x2 psa = 0ull, psb = 0ull;
       float ps0 = 0.f, ps1 = 0.f;
       uint32_t pk[16];
+      constexpr int NU = TK / 8;  // 16-byte units of 8 keys
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {  // 16-byte units of 8 keys
+      for (int u = 0; u < NU; ++u) {
         float pv[8];
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
@@ -536,14 +545,14 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_>::THREADS, 1)
         for (int e = 0; e < 4; ++e)
           pk[(u & 3) * 4 + e] = kBF16 ? tc::pack_bf16x2(pv[2 * e], pv[2 * e + 1])
                                       : tc::pack_f16x2(pv[2 * e], pv[2 * e + 1]);
-        constexpr int UPH = 16 / PH;  // 8-key units per P part
+        constexpr int UPH = NU / PH;  // 8-key units per P part
         if ((u & 3) == 3) {  // 32 keys = 16 columns packed: into TMEM
           if (t > 0 && u % UPH == 3) {  // part's first store: its P V of tile t-1 must be done
             ptx::mbar_wait(&o_full[g * PH + u / UPH], (t - 1) & 1);
             tc::fence_after_sync();
           }
           tc::tmem_st_32x32b_x16(p_tm + (u >> 2) * 16, pk);
-          if (PH > 1 && !kTcSelfIssue && u % UPH == UPH - 1 && u != 15) {
+          if (PH > 1 && !kTcSelfIssue && u % UPH == UPH - 1 && u != NU - 1) {
             // part complete: hand it to the tensor core
             tc::tmem_wait_st();
             tc::fence_before_sync();
