@@ -798,6 +798,13 @@ def main():
         "peak_source": f"148 SM x 128 FP32 lanes x 2 x {fmax:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
         "k4_ffma_measured": k4, "frac_of_k4": (per_gpu / k4) if k4 else None,
         "traffic": traffic, "traffic_workload": traffic_workload,
+        # the K/V (and Q, Y) streams: DRAM bytes of the ncu capture over this
+        # run's kernel time (the north star's HBM GB/s evidence; far below the
+        # HBM roofline: the kernel is FFMA-bound at n/4 flop per byte)
+        "hbm_gbs": (traffic / (hl["ms"] * 1e-3) / 1e9) if traffic else None,
+        "hbm_peak_gbs": float(peaks.get("hbm_gbs") or 6650.0),
+        "hbm_peak_source": "MEASURED_PEAKS hbm_gbs" if peaks.get("hbm_gbs") else
+                           "fallback 6.65 TB/s (B200_PROFILING.md)",
         "algorithmic_flops_per_launch": flops(B1, args.heads, args.n, args.n),
         "algorithmic_bytes_per_launch": 4 * B1 * args.heads * (args.n * 64 * 3 + args.n * 64),
         "kernel": "elsa::fwd_f32_kernel (" + hl["plan"] + ")",
