@@ -39,6 +39,7 @@ workload (whole 64-query tiles), and reports the same metric.
 from __future__ import annotations
 
 import argparse
+import datetime
 import glob
 import json
 import math
@@ -338,7 +339,11 @@ class Ctx:
             os.environ.setdefault("MASTER_PORT", "29533")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", str(self.world))
-            dist.init_process_group("nccl", device_id=self.dev)
+            # a failed rank must not park the others for NCCL's default 10
+            # minutes: the longest gap between collectives here is one C5
+            # KV-sharded step (~20 s at N = 2)
+            dist.init_process_group("nccl", device_id=self.dev,
+                                    timeout=datetime.timedelta(minutes=5))
             t = torch.ones(1, device=self.dev)
             dist.all_reduce(t)
             torch.cuda.synchronize()
