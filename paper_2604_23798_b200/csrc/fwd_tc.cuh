@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
           tc::fence_after_sync();
           if (lane == 0 && hh == 0) TC_MARK(8 + g, u, 1);
           issue_o(g, u, hh, leader);
+          if (lane == 0 && hh == 0) TC_MARK(8 + g, u, 3);  // issue returned
           nph[g] = hh + 1 == PH ? 0 : hh + 1;
           npv[g] = hh + 1 == PH ? u + 1 : u;
           int done = npv[0];
@@ -388,6 +389,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
           tc::fence_after_sync();
           if (lane == 0) TC_MARK(8 + g, t, 0);
           issue_s(g, t, leader);
+          if (lane == 0) TC_MARK(8 + g, t, 2);  // issue returned
           ns[g] = t + 1;
         }
       }
