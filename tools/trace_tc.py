@@ -39,6 +39,10 @@ for w in (0, 1, 4):
 print("S issue -> S ready (g0):", np.mean([a[0, t, 1] - a[8, t, 0] for t in range(8, 56)]))
 print("p_full -> PV issue (g0):", np.mean([a[8, t, 1] - a[0, t, 5] for t in range(8, 56)]))
 print("s_free -> S issue (g0):", np.mean([a[8, t + 1, 0] - a[0, t, 2] for t in range(8, 56)]))
+print("O wait before the first P store (warp 0, warp 4):",
+      np.mean([a[0, t, 7] - a[0, t, 6] for t in range(8, 56)]),
+      np.mean([a[4, t, 7] - a[4, t, 6] for t in range(8, 56)]),
+      "| max done -> O wait start:", np.mean([a[0, t, 6] - a[0, t, 3] for t in range(8, 56)]))
 print("S issue call duration (g0):", np.mean([a[8, t, 2] - a[8, t, 0] for t in range(8, 56)]))
 print("PV issue call duration (g0):", np.mean([a[8, t, 3] - a[8, t, 1] for t in range(8, 56)]))
 ev = sorted([(a[8 + g, t, k], f"{'S' if k == 0 else 'PV'}{g}({t})", a[8 + g, t, k + 2] - a[8 + g, t, k])
