@@ -182,6 +182,10 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
     synchronises and raises :class:`NumericalError` on a bad normalizer, the
     way the reference raises from ``scan_forward`` (engine.py:377-378).
     """
+    if (enable_gqa and isinstance(query, torch.Tensor) and isinstance(key, torch.Tensor)
+            and query.dim() >= 3 and key.dim() >= 3 and key.shape[-3] != query.shape[-3]):
+        return _gqa_folded(query, key, value, attn_mask, dropout_p, is_causal, scale,
+                           kv_splits, check_numerics, out)
     if (attn_mask is None and not dropout_p and not is_causal and out is None
             and not check_numerics):
         y = _fast_f32(query, key, value, scale, kv_splits)
@@ -203,8 +207,6 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
     orig_dim = query.dim()
     orig_shape = query.shape
     q, k, v = (_prep(_as_4d(t, n)) for t, n in ((query, "query"), (key, "key"), (value, "value")))
-    if enable_gqa and k.shape[1] != q.shape[1]:
-        raise ShapeError("grouped-query attention (enable_gqa with H_kv != H_q) is not supported")
     d = q.shape[-1]
     sc = (1.0 / math.sqrt(d)) if scale is None else float(scale)
     if not math.isfinite(sc):
@@ -254,6 +256,40 @@ def scaled_dot_product_attention(query, key, value, attn_mask=None, dropout_p=0.
     if orig_dim == 4 or out is not None:
         return y
     return y.reshape(*orig_shape[:-1], dv)
+
+
+def _gqa_folded(query, key, value, attn_mask, dropout_p, is_causal, scale, kv_splits,
+                check_numerics, out):
+    """Grouped-query attention (``enable_gqa``, H_q = g * H_kv; query head h
+    reads key/value head h // g, torch's repeat_interleave semantics) without
+    repeating K/V: the g query heads of one K/V head are folded into its query
+    rows, (B, H_kv, g * n_q, d) — a view of a contiguous query — so one launch
+    runs every group against its K/V once. Rows are independent, so the
+    result is the same as with the heads expanded."""
+    if value.dim() < 3 or value.shape[-3] != key.shape[-3]:
+        raise ShapeError("key and value must have the same number of heads")
+    # heads are dim -3 (torch's convention for enable_gqa); leading dims fold into B
+    q4, k4, v4 = (t.reshape(-1, *t.shape[-3:]) for t in (query, key, value))
+    if q4.shape[0] != k4.shape[0] or k4.shape[0] != v4.shape[0]:
+        raise ShapeError(f"batch dims differ: q {tuple(query.shape)}, k {tuple(key.shape)}, "
+                         f"v {tuple(value.shape)}")
+    B, Hq, n_q, d = q4.shape
+    Hk = k4.shape[1]
+    if Hk < 1 or Hq % Hk:
+        raise ShapeError(f"enable_gqa needs the query heads ({Hq}) to be a multiple of the "
+                         f"key/value heads ({Hk})")
+    g = Hq // Hk
+    qf = q4.reshape(B, Hk, g * n_q, d)
+    sc = (1.0 / math.sqrt(d)) if scale is None else scale
+    y = scaled_dot_product_attention(qf, k4, v4, attn_mask, dropout_p, is_causal, sc, False,
+                                     kv_splits=kv_splits, check_numerics=check_numerics)
+    y = y.reshape(*query.shape[:-1], v4.shape[-1])
+    if out is not None:
+        if tuple(out.shape) != tuple(y.shape) or out.dtype != y.dtype or out.device != y.device:
+            raise ShapeError("out must match the output's shape, dtype and device")
+        out.copy_(y)
+        return out
+    return y
 
 
 _FAST = {}   # (shapes, strides, kv_splits, device) -> (ElsaShape, ws bytes, scale, Y shape)

@@ -64,3 +64,18 @@ def test_shim_accepts_reference_config_objects_duck_typed():
     prob = scanattn_compat.AttentionProblem(T4(x), T4(x), T4(x))
     with pytest.raises(elsa.ShapeError):
         scanattn_compat.scan_forward(prob, FakeCfg())
+
+
+def test_gqa_fold_validates_heads_and_rejects_cpu():
+    # H_q not a multiple of H_kv
+    with pytest.raises(elsa.ShapeError, match="multiple"):
+        elsa.scaled_dot_product_attention(t(1, 6, 4, 8), t(1, 4, 4, 8), t(1, 4, 4, 8),
+                                          enable_gqa=True)
+    # key / value head counts differ
+    with pytest.raises(elsa.ShapeError, match="same number of heads"):
+        elsa.scaled_dot_product_attention(t(1, 4, 4, 8), t(1, 2, 4, 8), t(1, 1, 4, 8),
+                                          enable_gqa=True)
+    # a valid fold still has no CPU path
+    with pytest.raises(elsa.ShapeError, match="no CPU fallback"):
+        elsa.scaled_dot_product_attention(t(1, 4, 4, 8), t(1, 2, 4, 8), t(1, 2, 4, 8),
+                                          enable_gqa=True)

@@ -414,3 +414,43 @@ def test_split_workspace_alignment_odd_rows(n_q, n_kv, splits):
     V = rng.standard_normal((1, 3, n_kv, 64)).astype(np.float32)
     y = run(Q, K, V, kv_splits=splits)
     assert_bound(y, oracle.naive_attention(Q, K, V), n_kv, f"{n_q}x{n_kv}/{splits}")
+
+
+@pytest.mark.parametrize("shape_q,hk", [((2, 8, 300, 64), 2), ((1, 12, 128, 64), 4),
+                                        ((8, 200, 64), 2), ((2, 3, 4, 100, 32), 1)])
+def test_grouped_query_attention_matches_torch_semantics(shape_q, hk):
+    """enable_gqa (torch semantics: query head h reads K/V head h // g): the
+    query heads of one K/V head are folded into its rows, no K/V repeat;
+    checked against the FP64 oracle on repeat_interleave'd K/V."""
+    rng = np.random.default_rng(len(shape_q) * 100 + hk)
+    *lead, hq, n, d = shape_q
+    Q = rng.standard_normal(shape_q).astype(np.float32)
+    K = rng.standard_normal((*lead, hk, 257, d)).astype(np.float32)
+    V = rng.standard_normal((*lead, hk, 257, d)).astype(np.float32)
+    y = elsa.scaled_dot_product_attention(gpu(Q), gpu(K), gpu(V), enable_gqa=True,
+                                          check_numerics=True)
+    assert tuple(y.shape) == tuple(shape_q)
+    g = hq // hk
+    Ke = np.repeat(K, g, axis=-3).astype(np.float64)
+    Ve = np.repeat(V, g, axis=-3).astype(np.float64)
+    ref = oracle.naive_attention(Q.reshape(-1, hq, n, d).astype(np.float64),
+                                 Ke.reshape(-1, hq, 257, d), Ve.reshape(-1, hq, 257, d))
+    err = oracle.row_rel_err(y.reshape(-1, hq, n, d).cpu().numpy(), ref)
+    assert err.max() <= oracle.bound_threshold(257), err.max()
+    # 16-bit inputs take the same fold (K5)
+    yb = elsa.scaled_dot_product_attention(gpu(Q).bfloat16(), gpu(K).bfloat16(),
+                                           gpu(V).bfloat16(), enable_gqa=True)
+    tb = torch.nn.functional.scaled_dot_product_attention(
+        gpu(Q).bfloat16(), gpu(K).bfloat16(), gpu(V).bfloat16(), enable_gqa=True) \
+        if len(shape_q) == 4 else None
+    if tb is not None:
+        assert (yb.float() - tb.float()).abs().max().item() < 3e-2
+
+
+def test_grouped_query_attention_rejects_non_multiple_heads():
+    q = torch.randn(1, 6, 16, 64, device=DEV)
+    k = torch.randn(1, 4, 16, 64, device=DEV)
+    with pytest.raises(elsa.ShapeError):
+        elsa.scaled_dot_product_attention(q, k, k, enable_gqa=True)
+    with pytest.raises(elsa.ShapeError):  # without enable_gqa the head counts must match
+        elsa.scaled_dot_product_attention(q, k, k)
