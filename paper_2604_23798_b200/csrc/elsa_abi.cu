@@ -34,6 +34,12 @@ using namespace elsa;
 namespace {
 
 constexpr int kMaxDevices = 64;
+#ifndef ELSA_EXPERIMENTAL_W8R4
+#define ELSA_EXPERIMENTAL_W8R4 0  // the w8r4 experiment config (round2_notes.md)
+#endif
+#ifndef ELSA_EXPERIMENTAL_TC_TK64
+#define ELSA_EXPERIMENTAL_TC_TK64 0  // K5 with 64-key tiles at d = 128 (round2_notes.md)
+#endif
 #ifndef ELSA_W8R8_STAGES
 #define ELSA_W8R8_STAGES 3  // K/V ring depth of w8r8 (3: +0.5% at 8K-16K, tools/ab_time.py; w4r8 at 3 stages loses its second CTA per SM: 4K 54.6 -> 49.5)
 #endif
@@ -155,7 +161,8 @@ enum CfgId {
   kCfgW8R8D128V96 = 13, // 96 < d <= 128, 64 < dv <= 96
   kCfgW4R8D256V256 = 14,  // 128 < d <= 256, dv > 128: 256 V columns per CTA (one S per tile)
   kCfgW8R8Acc = 15,  // w8r8 with the two-level W accumulator (long per-CTA chains)
-  kCfgW8R4 = 16,     // 8 consumer warps x 8 rows (TQ 64): latency-bound small problems
+  kCfgW8R4 = 16,     // 8 consumer warps x 8 rows (TQ 64); experiment, built with
+                     // -DELSA_EXPERIMENTAL_W8R4=1 only (measured no faster, round2_notes.md)
   kCfgAuto = -1
 };
 int cfg_dv(int cfg) {
@@ -187,7 +194,9 @@ int cfg_from_name(const char* e) {
   if (e && !std::strcmp(e, "w8r8")) return int(kCfgW8R8);
   if (e && !std::strcmp(e, "w8r16")) return int(kCfgW8R16);
   if (e && !std::strcmp(e, "w8r8acc")) return int(kCfgW8R8Acc);
+#if ELSA_EXPERIMENTAL_W8R4
   if (e && !std::strcmp(e, "w8r4")) return int(kCfgW8R4);
+#endif
   return int(kCfgAuto);
 }
 // ELSA_FWD_CFG (or elsa_dev_force_config) forces one of the d <= 64 configurations
@@ -345,7 +354,11 @@ int cluster_slot(int cfg) { return cfg == kCfgW8R8 ? 1 : (cfg == kCfgW8R4 ? 2 : 
 
 int active_clusters(int cfg, int splits, DeviceCache* dc) {
   if (!dc || splits < 2 || splits > kMaxClusterSplits) return 0;
+#if ELSA_EXPERIMENTAL_W8R4
   if (cfg == kCfgW8R4) return max_active_clusters<8, 64, 2, 4>(splits, dc, cluster_slot(cfg));
+#else
+  if (cfg == kCfgW8R4) return 0;
+#endif
   return cfg == kCfgW8R8
              ? max_active_clusters<8, 64, ELSA_W8R8_STAGES, 8>(splits, dc, cluster_slot(cfg))
              : max_active_clusters<4, 64, ELSA_W4R8_STAGES, 8>(splits, dc, cluster_slot(cfg));
@@ -651,9 +664,11 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
                cudaStream_t stream) {
   const int splits = plan.splits;
   if (plan.cluster) {
+#if ELSA_EXPERIMENTAL_W8R4
     if (plan.cfg == kCfgW8R4)
       return launch_fwd_cfg<8, 64, 2, 4, 64, 64, true>(p, s, q_st, k_st, v_st, splits, bh_count,
                                                        kCfgW8R4, dc, stream);
+#endif
     if (plan.cfg == kCfgW8R8)
       return launch_fwd_cfg<8, 64, ELSA_W8R8_STAGES, 8, 64, 64, true>(
           p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8, dc, stream);
@@ -671,8 +686,12 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
       return launch_fwd_cfg<8, 64, ELSA_W8R8_STAGES, 8, 64, 64, false, true>(
           p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8Acc, dc, stream);
     case kCfgW8R4:
+#if ELSA_EXPERIMENTAL_W8R4
       return launch_fwd_cfg<8, 64, 2, 4>(p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R4, dc,
                                          stream);
+#else
+      return ELSA_ERR_SHAPE;
+#endif
     case kCfgW8R8D128:
       return launch_fwd_cfg<8, 64, 2, 8, 128>(p, s, q_st, k_st, v_st, splits, bh_count,
                                               kCfgW8R8D128, dc, stream);
@@ -1310,9 +1329,10 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
   // the 64-key-tile kernel (no aliasing, S_g(t+1) overlaps the exponentials):
   // measured slower (BF16 16K 975 vs 1224, 64K 922 vs 1096; faster only at
   // n = 1K, 409 vs 350 TFLOP/s; profiles/round2_tc_d128_tk64.txt)
+  // (built with -DELSA_EXPERIMENTAL_TC_TK64=1 only)
   static const int tc_tk = [] {
     const char* e = std::getenv("ELSA_TC_TK");
-    return e && std::atoi(e) == 64 ? 64 : 128;
+    return ELSA_EXPERIMENTAL_TC_TK64 && e && std::atoi(e) == 64 ? 64 : 128;
   }();
   const int kv_box = wide16 ? tc_tk : 128;
   CUtensorMap maps[3];
@@ -1368,13 +1388,16 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
   };
   const int base = kAttrSlots - 12;  // the last twelve slots
   int st;
+#if ELSA_EXPERIMENTAL_TC_TK64
   if (wide16 && tc_tk == 64 && groups == 2)
     st = bf16 ? launch(TcTraits<2, 128, 64>{}, fwd_tc_kernel<true, 2, 128, 64>, base + 11)
               : launch(TcTraits<2, 128, 64>{}, fwd_tc_kernel<false, 2, 128, 64>, base + 10);
   else if (wide16 && tc_tk == 64)
     st = bf16 ? launch(TcTraits<1, 128, 64>{}, fwd_tc_kernel<true, 1, 128, 64>, base + 9)
               : launch(TcTraits<1, 128, 64>{}, fwd_tc_kernel<false, 1, 128, 64>, base + 8);
-  else if (wide16 && groups == 2)
+  else
+#endif
+  if (wide16 && groups == 2)
     st = bf16 ? launch(TcTraits<2, 128>{}, fwd_tc_kernel<true, 2, 128>, base + 7)
               : launch(TcTraits<2, 128>{}, fwd_tc_kernel<false, 2, 128>, base + 6);
   else if (wide16)
