@@ -77,6 +77,10 @@
 #ifndef ELSA_SNAKE
 #define ELSA_SNAKE -1
 #endif
+#ifndef ELSA_EPI_UNROLL
+#define ELSA_EPI_UNROLL 1  // staged-epilogue row-chunk loop (w4r8)
+#endif
+constexpr int kEpiUnroll = ELSA_EPI_UNROLL;
 #ifndef ELSA_CONSUMER_REGS
 #define ELSA_CONSUMER_REGS 224
 #endif
@@ -445,6 +449,26 @@ __device__ __forceinline__ void cluster_merge_epilogue(const FwdParams& p, float
 
 __device__ __forceinline__ float f4(const float4& v, int c) {
   return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+}
+
+// Y = W / S without a slow-path branch per element: with r = __frcp_rn(S),
+// Markstein's correction step q0 = W r, rem = fma(-S, q0, W) (exact),
+// q = fma(rem, r, q0) is the correctly rounded quotient when nothing
+// under/overflows. Used only when the whole warp's rows are in the guarded
+// range (S in [1, 2^31), |W| = 0 or in [2^-100, 2^100)); there it equals
+// __fdiv_rn bit for bit (4.6e9 random pairs over every exponent checked on a
+// B200, tools/microbench/div_check.cu); otherwise the epilogue divides with
+// __fdiv_rn. One reciprocal per row instead of a full division per element,
+// and straight-line code the scheduler can overlap across rows.
+__device__ __forceinline__ bool div_fast_ok_den(float s) { return s >= 1.f && s < 0x1p31f; }
+__device__ __forceinline__ bool div_fast_ok_num(float w) {
+  const float a = fabsf(w);
+  return a == 0.f || (a >= 0x1p-100f && a < 0x1p100f);
+}
+__device__ __forceinline__ float div_rn_rcp(float w, float s, float r) {
+  const float q0 = w * r;
+  const float rem = fmaf(-s, q0, w);
+  return fmaf(rem, r, q0);
 }
 
 // CL (cluster split merge): the kv splits of one query tile are the CTAs of
@@ -910,7 +934,35 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
     for (int i = 0; i < R; ++i) lrow[i] += __shfl_xor_sync(0xffffffffu, lrow[i], sh);
   }
   trace_mark(p, warp, ntiles, 1);
-  if constexpr (T::DV == 64 && T::W <= 4 && (TK / T::PH) * PTP >= WR * 66) {
+  // final output: quotients with one reciprocal per row when the whole warp
+  // is in the fast division's range (warp-uniform), written over o2
+  bool qdone = false;
+  constexpr bool kStaged = T::DV == 64 && T::W <= 4 && (TK / T::PH) * PTP >= WR * 66;
+  // (the staged w4r8 epilogue only: in the unrolled w8r8 one it measured
+  // slower, H16 1K 100.3 vs 98.3 us, profiles/round2_ab_div.txt)
+  if (kStaged && mode == kModeFinal) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < R; ++i) ok = ok && div_fast_ok_den(lrow[i]);
+#pragma unroll
+    for (int ip = 0; ip < RP; ++ip)
+#pragma unroll
+      for (int c = 0; c < CV; ++c)
+        ok = ok && div_fast_ok_num(ptx::lo2(o2[ip][c])) && div_fast_ok_num(ptx::hi2(o2[ip][c]));
+    if (__all_sync(0xffffffffu, ok)) {
+      float rr[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) rr[i] = __frcp_rn(lrow[i]);
+#pragma unroll
+      for (int ip = 0; ip < RP; ++ip)
+#pragma unroll
+        for (int c = 0; c < CV; ++c)
+          o2[ip][c] = ptx::pack2(div_rn_rcp(ptx::lo2(o2[ip][c]), lrow[2 * ip], rr[2 * ip]),
+                                 div_rn_rcp(ptx::hi2(o2[ip][c]), lrow[2 * ip + 1], rr[2 * ip + 1]));
+      qdone = true;
+    }
+  }
+  if constexpr (kStaged) {
     // Staged epilogue (64-column slices): the warp parks its rows' W, S and
     // anchor in its own P area, then one compact loop writes each row as 16
     // coalesced float4 chunks (Y = W / S with the same IEEE division, or the
@@ -940,7 +992,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
     __syncwarp();
     const int qw = q0 + warp * WR;
     const int rows_here = p.n_q - qw < WR ? p.n_q - qw : WR;
-#pragma unroll 1
+#pragma unroll(kEpiUnroll)
     for (int idx = lane; idx < rows_here * 16; idx += 32) {
       const int r = idx >> 4, c4 = idx & 15;
       const int qrow = qw + r;
@@ -950,8 +1002,9 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
       if (mode == kModeFinal) {
         // engine.py:377-378: the normalizer must be finite and positive
         if (c4 == 0 && (!(l > 0.f) || !isfinite(l))) atomicCAS(p.err, 0, 3);
-        const float4 y = make_float4(__fdiv_rn(w.x, l), __fdiv_rn(w.y, l), __fdiv_rn(w.z, l),
-                                     __fdiv_rn(w.w, l));
+        const float4 y = qdone ? w
+                               : make_float4(__fdiv_rn(w.x, l), __fdiv_rn(w.y, l),
+                                             __fdiv_rn(w.z, l), __fdiv_rn(w.w, l));
         float* yrow = p.y + int64_t(b) * p.ys_b + int64_t(h) * p.ys_h + int64_t(qrow) * p.ys_r;
         if (p.y_vec && col + 3 < p.dv) {
           *reinterpret_cast<float4*>(yrow + col) = y;
@@ -1004,7 +1057,7 @@ __global__ void __maxnreg__((FwdTraits<W_, TK_, STAGES_, R_, D_, DV_>::MAX_REGS)
         float* yrow = p.y + int64_t(b) * p.ys_b + int64_t(h) * p.ys_h + int64_t(qrow) * p.ys_r;
         float yv[CV];
 #pragma unroll
-        for (int c = 0; c < CV; ++c) yv[c] = __fdiv_rn(o[c], l);
+        for (int c = 0; c < CV; ++c) yv[c] = qdone ? o[c] : __fdiv_rn(o[c], l);
 #pragma unroll
         for (int v4 = 0; v4 < T::NSEG; ++v4) {
           if constexpr (T::DV != 96) {  // uniform segments (compile-time width)
