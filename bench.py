@@ -89,6 +89,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--sampled-parity", action="store_true",
+                    help="N = 1: check 64 sampled rows instead of every row of the timed output")
     ap.add_argument("--long", default="c4,c5",
                     help="long-context configs to time at every N (comma list of c4, c5; "
                          "'none' to skip)")
@@ -437,6 +439,34 @@ def sampled_parity(q, k, v, y_rows, row_lo, rows_wanted, seed):
     return (max(errs) if errs else 0.0), len(errs)
 
 
+def full_parity(q, k, v, y_rows):
+    """Every output row against the FP64 oracle (oracles.py:92-98 restated in
+    numpy float64, query rows in chunks); max per-row relative L2 error
+    (verify.py:336-338) and the row count."""
+    import torch
+    f64 = torch.float64
+    B, H, n_q, d = q.shape
+    sc = 1.0 / math.sqrt(d)
+    Y = y_rows.reshape(B, H, n_q, -1)
+    worst, rows = 0.0, 0
+    for b in range(B):
+        for h in range(H):
+            K = k[b, h].to(f64).cpu().numpy()
+            V = v[b, h].to(f64).cpu().numpy()
+            Qh = q[b, h].to(f64).cpu().numpy()
+            Yh = Y[b, h].to(f64).cpu().numpy()
+            for r0 in range(0, n_q, 2048):
+                s = (Qh[r0:r0 + 2048] @ K.T) * sc
+                s -= s.max(axis=1, keepdims=True)
+                np.exp(s, out=s)
+                ref = (s @ V) / s.sum(axis=1, keepdims=True)
+                e = np.linalg.norm(Yh[r0:r0 + 2048] - ref, axis=1) / np.linalg.norm(ref, axis=1)
+                worst = max(worst, float(e.max()))
+                rows += e.size
+            del K, V, Qh, Yh
+    return worst, rows
+
+
 def _parity_block(ctx, err, rows, n_kv):
     err = ctx.max_over_ranks(err)
     rows = int(ctx.sum_over_ranks(rows))
@@ -503,8 +533,15 @@ def headline(args, ctx, elsa, edist):
     value = fl / (ms * 1e-3) / 1e12
     parity = None
     if not args.no_parity:
-        err, cnt = sampled_parity(q, k, v, y_rows, lo, max(8, 64 // world), seed=rank + 1)
-        parity = _parity_block(ctx, err, cnt, n)
+        if world == 1 and not args.sampled_parity:
+            # every row of the timed output against the FP64 oracle (~20 s of
+            # host BLAS at 16K)
+            err, cnt = full_parity(q, k, v, y_rows)
+            parity = _parity_block(ctx, err, cnt, n)
+            parity["rows_checked"] = "all"
+        else:
+            err, cnt = sampled_parity(q, k, v, y_rows, lo, max(8, 64 // world), seed=rank + 1)
+            parity = _parity_block(ctx, err, cnt, n)
     plan = elsa.describe_plan(q[:1], k[:1], v[:1])
     return dict(q=q, k=k, v=v, Bg=Bg, fl=fl, ms=ms, value=value, clocks=clock_info,
                 launches=timed_launches, parity=parity, plan=plan, chunks=chunks,

@@ -127,3 +127,20 @@ def test_chain_cap_holds_when_workspace_budget_binds():
     big = torch.empty(1, 1, 1, 64, device=DEV).expand(1, 1, 1 << 26, 64)
     plan = elsa.describe_plan(q[:, :, :1024], big, big)
     assert "chain_tiles=32768" in plan, plan
+
+
+def test_every_row_fp64_at_the_headline_size():
+    """C3 at 16K (the bench headline): all 262144 output rows of the auto
+    plan within u * L(16384, 128) * 8 of the FP64 oracle (oracles.py:74-104),
+    not a sample (~20 s of host FP64)."""
+    g = torch.Generator(device=DEV)
+    g.manual_seed(1234)
+    q, k, v = (torch.randn(1, 16, 16384, 64, device=DEV, generator=g) for _ in range(3))
+    y = elsa.scaled_dot_product_attention(q, k, v, check_numerics=True).cpu().numpy()
+    Q, K, V = (t.cpu().numpy() for t in (q, k, v))
+    worst = 0.0
+    for h in range(16):
+        ref = oracle.naive_attention_rows_fp64(Q[:, h:h + 1], K[:, h:h + 1], V[:, h:h + 1],
+                                               rows_per_chunk=2048)[0, 0]
+        worst = max(worst, float(oracle.row_rel_err(y[0, h], ref).max()))
+    assert worst <= oracle.bound_threshold(16384), worst
