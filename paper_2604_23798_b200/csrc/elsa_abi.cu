@@ -37,6 +37,9 @@ constexpr int kMaxDevices = 64;
 #ifndef ELSA_EXPERIMENTAL_W8R4
 #define ELSA_EXPERIMENTAL_W8R4 0  // the w8r4 experiment config (round2_notes.md)
 #endif
+#ifndef ELSA_EXPERIMENTAL_TC_CS2
+#define ELSA_EXPERIMENTAL_TC_CS2 0  // K5 with two softmax warps per row (round2_notes.md)
+#endif
 #ifndef ELSA_EXPERIMENTAL_TC_TK64
 #define ELSA_EXPERIMENTAL_TC_TK64 0  // K5 with 64-key tiles at d = 128 (round2_notes.md)
 #endif
@@ -49,7 +52,7 @@ constexpr int kMaxDevices = 64;
 #ifndef ELSA_W4R8_STAGES
 #define ELSA_W4R8_STAGES 2
 #endif
-constexpr int kAttrSlots = 46;
+constexpr int kAttrSlots = 48;
 constexpr int kMaxSplits = kMergeMaxParts;
 constexpr double kLog2e = 1.4426950408889634074;
 
@@ -1386,7 +1389,14 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
         p, maps[0], maps[1], maps[2]);
     return ELSA_OK;
   };
-  const int base = kAttrSlots - 12;  // the last twelve slots
+  const int base = kAttrSlots - 14;  // the last fourteen slots
+  // ELSA_TC_CS=2 (experiment, built with -DELSA_EXPERIMENTAL_TC_CS2=1): two
+  // softmax warps per row (column split), d <= 64 two-group CTAs — measured
+  // slower (BF16 16K 801 vs 905 TFLOP/s, profiles/round2_tc_cs2.txt)
+  static const int tc_cs = [] {
+    const char* e = std::getenv("ELSA_TC_CS");
+    return ELSA_EXPERIMENTAL_TC_CS2 && e && std::atoi(e) == 2 ? 2 : 1;
+  }();
   int st;
 #if ELSA_EXPERIMENTAL_TC_TK64
   if (wide16 && tc_tk == 64 && groups == 2)
@@ -1403,6 +1413,11 @@ int elsa_fwd_f16(const void* q, const void* k, const void* v, void* y, const els
   else if (wide16)
     st = bf16 ? launch(TcTraits<1, 128>{}, fwd_tc_kernel<true, 1, 128>, base + 5)
               : launch(TcTraits<1, 128>{}, fwd_tc_kernel<false, 1, 128>, base + 4);
+#if ELSA_EXPERIMENTAL_TC_CS2
+  else if (groups == 2 && tc_cs == 2)
+    st = bf16 ? launch(TcTraits<2, 64, 128, 2>{}, fwd_tc_kernel<true, 2, 64, 128, 2>, base + 13)
+              : launch(TcTraits<2, 64, 128, 2>{}, fwd_tc_kernel<false, 2, 64, 128, 2>, base + 12);
+#endif
   else if (groups == 2)
     st = bf16 ? launch(TcTraits<2>{}, fwd_tc_kernel<true, 2>, base + 3)
               : launch(TcTraits<2>{}, fwd_tc_kernel<false, 2>, base + 2);

@@ -169,9 +169,15 @@ constexpr float kRescaleLog2 = 8.f;
 // of both groups fit the 512 TMEM columns without aliasing, so S_g(t+1) is
 // issued as soon as S_g(t) is in registers (overlapping the exponentials) as
 // at D = 64, instead of after P_g(t) V.
-template <int GROUPS, int D_ = 64, int TK_ = 128>
+//
+// CS_ = 2 (experiment, D = 64 two-group CTAs): each query row's 128 scores are
+// split over two softmax warps on the same TMEM lane quarter (64 columns
+// each; the row max exchanged through shared memory per tile), so four
+// softmax warps share every SM sub-partition instead of two.
+template <int GROUPS, int D_ = 64, int TK_ = 128, int CS_ = 1>
 struct TcTraits {
-  static constexpr int TQ = 128, TK = TK_, D = D_;
+  static constexpr int TQ = 128, TK = TK_, D = D_, CS = CS_;
+  static_assert(CS == 1 || (CS == 2 && D == 64 && TK == 128 && GROUPS == 2), "column split");
   static_assert(D == 64 || D == 128, "head width");
   static_assert(TK == 128 || (TK == 64 && D == 128), "key tile");
   static constexpr bool kAliasP = D == 128 && TK == 128;
@@ -195,8 +201,11 @@ struct TcTraits {
   static constexpr int PH = kTcSelfIssue ? 1 : ELSA_TC_PSPLIT;
   static_assert(PH == 1 || PH == 2 || PH == 4, "P parts");
   static constexpr int NBAR = 1 + 2 * STAGES + (2 + 2 * PH) * GROUPS;
-  static constexpr size_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16 + 1024;  // + 1024 alignment slack
-  static constexpr int SOFTMAX_WARPS = 4 * GROUPS;
+  // CS = 2: row-max / row-sum exchange slots, [3 * GROUPS * 4][64] floats
+  static constexpr int OFF_XCH = ((OFF_BAR + NBAR * 8 + 16) + 15) / 16 * 16;
+  static constexpr int XCH_BYTES = CS == 2 ? 3 * GROUPS * 4 * 64 * 4 : 0;
+  static constexpr size_t SMEM_BYTES = OFF_XCH + XCH_BYTES + 1024;  // + 1024 alignment slack
+  static constexpr int SOFTMAX_WARPS = 4 * GROUPS * CS;
   static constexpr int TMA_WARP = SOFTMAX_WARPS, MMA_WARP = SOFTMAX_WARPS + 1;
   // GROUPS = 2: a whole third warpgroup (TMA, MMA, two idle warps) so setmaxnreg
   // can hand its registers to the softmax warpgroups; 12 warps launch at 168
@@ -205,8 +214,13 @@ struct TcTraits {
   // more than is freed blocks the .inc forever.
   static constexpr bool kRegSplit = GROUPS == 2;
   static constexpr int THREADS = kRegSplit ? (SOFTMAX_WARPS + 4) * 32 : (SOFTMAX_WARPS + 2) * 32;
-  static constexpr int SOFTMAX_REGS = 232, OTHER_REGS = 40;
-  static_assert(!kRegSplit || 2 * (SOFTMAX_REGS - 168) <= 168 - OTHER_REGS, "setmaxnreg budget");
+  // launch allocation per thread (the register file / THREADS, granule 8):
+  // 12 warps 168, 20 warps (CS = 2) 96
+  static constexpr int LAUNCH_REGS = (65536 / THREADS) / 8 * 8 > 255 ? 255 : (65536 / THREADS) / 8 * 8;
+  static constexpr int SOFTMAX_REGS = CS == 2 ? 104 : 232, OTHER_REGS = 40;
+  static_assert(!kRegSplit || (SOFTMAX_WARPS / 4) * (SOFTMAX_REGS - LAUNCH_REGS) <=
+                                  LAUNCH_REGS - OTHER_REGS,
+                "setmaxnreg budget");
   static constexpr uint32_t S_COL = 0;             // group g: S at TK g
   static constexpr uint32_t O_COL = TK * GROUPS;   // group g: W (P V accumulator) at O_COL + D g
   // group g: P (16-bit, two per 32-bit column) at P_COL + P_STRIDE g — the A
@@ -221,12 +235,12 @@ struct TcTraits {
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
-template <bool kBF16, int GROUPS, int D_ = 64, int TK_ = 128>
-__global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
+template <bool kBF16, int GROUPS, int D_ = 64, int TK_ = 128, int CS_ = 1>
+__global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_, CS_>::THREADS, 1)
     fwd_tc_kernel(const __grid_constant__ TcParams p, const __grid_constant__ CUtensorMap tmQ,
                   const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV) {
-  using T = TcTraits<GROUPS, D_, TK_>;
+  using T = TcTraits<GROUPS, D_, TK_, CS_>;
   extern __shared__ unsigned char smem_dyn[];
   // 1024-byte alignment for the 128B-swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -259,9 +273,9 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
     }
     for (int g = 0; g < GROUPS; ++g) {
       ptx::mbar_init(&s_full[g], 1);
-      ptx::mbar_init(&s_free[g], 128);
+      ptx::mbar_init(&s_free[g], 128 * T::CS);
       for (int hh = 0; hh < PH; ++hh) {
-        ptx::mbar_init(&p_full[g * PH + hh], 128);
+        ptx::mbar_init(&p_full[g * PH + hh], 128 * T::CS);
         ptx::mbar_init(&o_full[g * PH + hh], 1);
       }
     }
@@ -437,16 +451,24 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
   } else if (warp < T::SOFTMAX_WARPS) {
     // ------------- softmax + combine + epilogue (one warpgroup per query tile) -------------
     if constexpr (T::kRegSplit) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(T::SOFTMAX_REGS));
-    const int g = warp >> 2;
+    constexpr int CS = T::CS;
+    const int g = warp / (4 * CS);
+    const int cpart = (warp % (4 * CS)) / 4;  // this warp's column part of the row (CS = 2)
     const int row = (warp & 3) * 32 + lane;
     const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-    const uint32_t s_tm = tmem + lane_base + T::S_COL + g * T::TK;
+    const uint32_t s_tm = tmem + lane_base + T::S_COL + g * T::TK + cpart * (T::TK / CS);
     const uint32_t o_tm = tmem + lane_base + T::O_COL + g * T::D;
+    // CS = 2: per-tile row-max exchange between the two warps of a lane quarter
+    // (double-buffered by tile parity; named barrier 1 + 4 g + quarter, 64 threads)
+    float* xmax = reinterpret_cast<float*>(smem + T::OFF_XCH);
+    auto pair_sync = [&]() {
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + 4 * g + (warp & 3)) : "memory");
+    };
     const float c2 = p.c;
     const float cs = p.neg ? -c2 : c2;  // exponent = s_raw * cs - m
     float m_run = -CUDART_INF_F;        // log2-domain anchor
     float l_run = 0.f;
-    const uint32_t p_tm = tmem + lane_base + T::P_COL + g * T::P_STRIDE;
+    const uint32_t p_tm = tmem + lane_base + T::P_COL + g * T::P_STRIDE + cpart * (T::TK / CS / 2);
     // self-issue: warp 0 of the group issues the group's MMAs after a
     // group-wide named barrier (id 1 + g) instead of signalling the MMA warp
     const bool issuer = kTcSelfIssue && (warp & 3) == 0;
@@ -466,7 +488,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
       ptx::mbar_wait(&s_full[g], t & 1);
       if (lane == 0) TC_MARK(warp, t, 1);
       tc::fence_after_sync();
-      constexpr int TK = T::TK;
+      constexpr int TK = T::TK / CS;  // this warp's keys of the tile
       float s[TK];
 #pragma unroll
       for (int ch = 0; ch < TK / 32; ++ch) {
@@ -489,8 +511,8 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
         ptx::mbar_arrive(&s_free[g]);
       }
       if (lane == 0) TC_MARK(warp, t, 2);
-      const int kv_hi = p.n_kv - t * T::TK;  // valid keys in this tile
-      if (kv_hi < T::TK) {                   // tail tile (warp-uniform): mask past n_kv
+      const int kv_hi = p.n_kv - t * T::TK - cpart * TK;  // valid keys in this warp's part
+      if (kv_hi < TK) {                   // tail tile (warp-uniform): mask past n_kv
 #pragma unroll
         for (int i = 0; i < TK; ++i)
           if (i >= kv_hi) s[i] = p.neg ? CUDART_INF_F : -CUDART_INF_F;
@@ -518,6 +540,12 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
         m_tile = fmaxf(fmaxf(fmaxf(acc[0], acc[1]), fmaxf(acc[2], acc[3])),
                        fmaxf(fmaxf(acc[4], acc[5]), fmaxf(acc[6], acc[7]))) * c2;
       }
+      if constexpr (CS == 2) {  // the row's other half
+        float* slot = xmax + ((t & 1) * GROUPS * 4 + g * 4 + (warp & 3)) * 64;
+        slot[cpart * 32 + lane] = m_tile;
+        pair_sync();
+        m_tile = fmaxf(m_tile, slot[(cpart ^ 1) * 32 + lane]);
+      }
       // deferred anchor: move only when the tile max exceeds it by > kRescaleLog2
       const bool move = m_tile > m_run + kRescaleLog2;
       const float m_new = move ? m_tile : m_run;
@@ -534,7 +562,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
         tc::fence_after_sync();
         {
 #pragma unroll
-          for (int ch = 0; ch < T::D / 32; ++ch) {
+          for (int ch = cpart * (T::D / 32 / CS); ch < (cpart + 1) * (T::D / 32 / CS); ++ch) {
             uint32_t r[32];
             tc::tmem_ld_32x32b_x32(o_tm + ch * 32, r);
             tc::tmem_wait_ld();
@@ -629,22 +657,30 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
       if (lane == 0) TC_MARK(warp, t, 5);
     }
     // ---- epilogue: Y = W / S (engine.py:375-382) in the input's 16-bit format ----
-    float w[T::D];
+    if constexpr (CS == 2) {  // the row sum is split over the pair
+      float* slot = xmax + (2 * GROUPS * 4 + g * 4 + (warp & 3)) * 64;
+      slot[cpart * 32 + lane] = l_run;
+      pair_sync();
+      l_run = slot[lane] + slot[32 + lane];
+    }
+    constexpr int DC = T::D / CS;  // this warp's output columns
+    const int col0 = cpart * DC;
+    float w[DC];
     if (ntiles > 0) {
 #pragma unroll
       for (int hh = 0; hh < PH; ++hh) ptx::mbar_wait(&o_full[g * PH + hh], (ntiles - 1) & 1);
       tc::fence_after_sync();
 #pragma unroll
-      for (int ch = 0; ch < T::D / 32; ++ch) {
+      for (int ch = 0; ch < DC / 32; ++ch) {
         uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(o_tm + ch * 32, r);
+        tc::tmem_ld_32x32b_x32(o_tm + col0 + ch * 32, r);
         tc::tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 32; ++i) w[ch * 32 + i] = __uint_as_float(r[i]);
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < T::D; ++i) w[i] = 0.f;
+      for (int i = 0; i < DC; ++i) w[i] = 0.f;
     }
     const int qrow = q0 + g * T::TQ + row;
     if (qrow < p.n_q) {
@@ -652,9 +688,10 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
       const float inv = 1.f / l_run;
       unsigned char* yrow = reinterpret_cast<unsigned char*>(p.y) +
                             2 * (int64_t(b) * p.ys_b + int64_t(h) * p.ys_h + int64_t(qrow) * p.ys_r);
+      yrow += 2 * col0;
 #pragma unroll
-      for (int u = 0; u < T::D / 8; ++u) {
-        if (8 * u >= p.dv) break;
+      for (int u = 0; u < DC / 8; ++u) {
+        if (col0 + 8 * u >= p.dv) break;
         uint4 pk;
         const float* x = w + 8 * u;
         if constexpr (kBF16) {
@@ -668,13 +705,13 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_>::THREADS, 1)
           pk.z = tc::pack_f16x2(x[4] * inv, x[5] * inv);
           pk.w = tc::pack_f16x2(x[6] * inv, x[7] * inv);
         }
-        if (p.y_vec && 8 * u + 8 <= p.dv) {
+        if (p.y_vec && col0 + 8 * u + 8 <= p.dv) {
           *reinterpret_cast<uint4*>(yrow + 16 * u) = pk;
         } else {  // narrow / unaligned output rows: 16-bit element stores
           const uint32_t wds[4] = {pk.x, pk.y, pk.z, pk.w};
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            if (8 * u + e < p.dv)
+            if (col0 + 8 * u + e < p.dv)
               reinterpret_cast<uint16_t*>(yrow)[8 * u + e] =
                   uint16_t(e & 1 ? wds[e >> 1] >> 16 : wds[e >> 1] & 0xffffu);
         }
