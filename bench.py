@@ -521,9 +521,17 @@ def headline(args, ctx, elsa, edist):
     # sampling steadily before the timed region opens
     clocks = ClockSampler(ctx.local)
     clocks.start()
-    for _ in range(warm):
+    # at least W steps and at least ~0.5 s of GPU work, so the SM clocks have
+    # left the idle state before timing (the reported warmup is the count run)
+    t_warm = time.time()
+    done = 0
+    # (N > 1: a fixed count, the KV-sharded steps hold collectives)
+    while done < warm or (not ctx.distributed and time.time() - t_warm < 0.5):
         step()
-    torch.cuda.synchronize()
+        done += 1
+        if done >= warm:
+            torch.cuda.synchronize()
+    warm = done
     clocks.wait_first(timeout=10.0)
     launches[0] = 0
     ms, (lo, y_rows) = ctx.timed(step, args.steps)
