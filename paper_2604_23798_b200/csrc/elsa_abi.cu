@@ -362,9 +362,14 @@ int active_clusters(int cfg, int splits, DeviceCache* dc) {
 #else
   if (cfg == kCfgW8R4) return 0;
 #endif
+#if ELSA_W8R8_REGSPLIT  // (experiment: the register-split w8r8 has no cluster form)
+  if (cfg == kCfgW8R8) return 0;
+  return max_active_clusters<4, 64, ELSA_W4R8_STAGES, 8>(splits, dc, cluster_slot(cfg));
+#else
   return cfg == kCfgW8R8
              ? max_active_clusters<8, 64, ELSA_W8R8_STAGES, 8>(splits, dc, cluster_slot(cfg))
              : max_active_clusters<4, 64, ELSA_W4R8_STAGES, 8>(splits, dc, cluster_slot(cfg));
+#endif
 }
 
 Plan plan_for(const elsa_shape* sh, int64_t kv_len, int requested, int sms,
@@ -672,9 +677,11 @@ int launch_fwd(FwdParams& p, const elsa_shape* s, int64_t q_st[3], int64_t k_st[
       return launch_fwd_cfg<8, 64, 2, 4, 64, 64, true>(p, s, q_st, k_st, v_st, splits, bh_count,
                                                        kCfgW8R4, dc, stream);
 #endif
+#if !ELSA_W8R8_REGSPLIT
     if (plan.cfg == kCfgW8R8)
       return launch_fwd_cfg<8, 64, ELSA_W8R8_STAGES, 8, 64, 64, true>(
           p, s, q_st, k_st, v_st, splits, bh_count, kCfgW8R8, dc, stream);
+#endif
     return launch_fwd_cfg<4, 64, ELSA_W4R8_STAGES, 8, 64, 64, true>(
         p, s, q_st, k_st, v_st, splits, bh_count, kCfgW4R8, dc, stream);
   }

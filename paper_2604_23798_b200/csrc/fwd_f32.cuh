@@ -218,7 +218,11 @@ struct FwdTraits {
   // round-robin), so 9 warps would cap every warp at 168 registers.
   // DV = 128: the 128-column W accumulator needs the same register split
   // (with 8 consumer warps; 4 consumer warps already launch at 255).
-  static constexpr bool kRegSplit = R >= 16 || (DV > 64 && W > 4);
+#ifndef ELSA_W8R8_REGSPLIT
+#define ELSA_W8R8_REGSPLIT 0  // experiment: producer warpgroup + 224-register consumers for w8r8
+#endif
+  static constexpr bool kRegSplit =
+      R >= 16 || (DV > 64 && W > 4) || (ELSA_W8R8_REGSPLIT && W == 8 && R == 8 && D <= 64);
   static constexpr int PRODUCER_WARPS = kRegSplit ? 4 : 1;
   static constexpr int THREADS = (W + PRODUCER_WARPS) * 32;
   // two CTAs per SM when a 4-warp CTA's shared memory leaves room for two
