@@ -99,14 +99,6 @@ constexpr bool kTcPackedG2 = ELSA_TC_PACKED_G2 != 0;
 // 25% 1230, 31% 1220, 37.5% 1198 TFLOP/s
 #define ELSA_TC_POLY_EXTRA_D128 0
 #endif
-// MMA-warp event order (experiments, profiles/round2_tc_order.txt): 0 = per
-// group P V then S (default), 1 = every ready P V before any S (BF16 16K 1.74
-// vs 1.21 ms: S_g(t+1) must overlap the exponentials), 2 = per group S then P V
-#ifndef ELSA_TC_ORDER
-#define ELSA_TC_ORDER 0
-#endif
-constexpr bool kTcPvFirst = ELSA_TC_ORDER == 1;
-constexpr bool kTcSFirst = ELSA_TC_ORDER == 2;
 #ifndef ELSA_TC_POLY_DEG
 #define ELSA_TC_POLY_DEG 3
 #endif
@@ -384,23 +376,10 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_, CS_>::THREADS, 1)
     for (int g = 0; g < GROUPS; ++g) ns[g] = npv[g] = nph[g] = 0;
     int kv_released = 0;  // tiles whose K/V stage was handed back
     while (kv_released < ntiles) {
-      // P V issues first (they are on the softmax's path: the next P store
-      // waits for them); an S issue only when no P V is ready (ELSA_TC_PV_FIRST)
-      bool issued_pv = false;
+      // (issue order measured: per group P V then S is best; every ready P V
+      // first, or S before P V, measured slower — profiles/round2_tc_order.txt)
 #pragma unroll
       for (int g = 0; g < GROUPS; ++g) {
-        if (kTcSFirst) {
-          const int t = ns[g];
-          if (t < ntiles && (!T::kAliasP || npv[g] >= t) &&
-              (t == 0 || ready(&s_free[g], (t - 1) & 1)) &&
-              ready(&kv_full[t % T::STAGES], (t / T::STAGES) & 1)) {
-            tc::fence_after_sync();
-            if (lane == 0) TC_MARK(8 + g, t, 0);
-            issue_s(g, t, leader);
-            if (lane == 0) TC_MARK(8 + g, t, 2);
-            ns[g] = t + 1;
-          }
-        }
         const int u = npv[g], hh = nph[g];
         if (u < ns[g] && ready(&p_full[g * PH + hh], u & 1)) {  // P V first: on the softmax's path
           tc::fence_after_sync();
@@ -417,9 +396,7 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_, CS_>::THREADS, 1)
             __syncwarp();
             ++kv_released;
           }
-          issued_pv = true;
         }
-        if (kTcPvFirst || kTcSFirst) continue;
         const int t = ns[g];
         // (P aliased over S: S_g(t) only after P_g(t-1) V has been issued)
         if (t < ntiles && (!T::kAliasP || npv[g] >= t) &&
@@ -430,21 +407,6 @@ __global__ void __launch_bounds__(TcTraits<GROUPS, D_, TK_, CS_>::THREADS, 1)
           issue_s(g, t, leader);
           if (lane == 0) TC_MARK(8 + g, t, 2);  // issue returned
           ns[g] = t + 1;
-        }
-      }
-      if (!kTcPvFirst || issued_pv) continue;
-#pragma unroll
-      for (int g = 0; g < GROUPS; ++g) {
-        const int t = ns[g];
-        if (t < ntiles && (!T::kAliasP || npv[g] >= t) &&
-            (t == 0 || ready(&s_free[g], (t - 1) & 1)) &&
-            ready(&kv_full[t % T::STAGES], (t / T::STAGES) & 1)) {
-          tc::fence_after_sync();
-          if (lane == 0) TC_MARK(8 + g, t, 0);
-          issue_s(g, t, leader);
-          if (lane == 0) TC_MARK(8 + g, t, 2);  // issue returned
-          ns[g] = t + 1;
-          break;  // re-check the P V barriers before the next S
         }
       }
     }
